@@ -1,0 +1,172 @@
+/*
+ * srlu.h — C ABI of the B200 (sm_100a) sparse randomized LU library
+ * (libsrlu.so).  Plain pointers and sizes only; every device buffer is
+ * owned by the caller (e.g. the torch caching allocator), every call is
+ * asynchronous on the caller's stream, nothing allocates, no C++ exception
+ * crosses the boundary.  Return 0 (SRLU_OK) or a negative SRLU_ERR_*;
+ * srlu_last_error() returns a thread-local message for the last failure.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/sparselu/):
+ *   srlu_seed_key / srlu_draw_sem / srlu_draw_fast_transform
+ *        <- sketch.py:42-43 (_rng), :103-114 (build_sem),
+ *           :214-235 (build_fast_transform), :269-278 (build_composite)
+ *   srlu_sem_plan             <- the accumulation order of _fast.pyx:44-90
+ *                                (bucket-grouped, ascending source index)
+ *   srlu_sketch_right_dense   <- sketch.py:362-368 apply_sketch_right =
+ *                                _fast.pyx:44-54 sem_gather_dense +
+ *                                sketch.py:322-335 _fast_adjoint_right +
+ *                                _fast.pyx:23-41 fwht_rows (fused)
+ *   srlu_sketch_right_csr     <- same with _fast.pyx:57-68 sem_gather_csc
+ *   srlu_sem_gather_dense     <- _kernels.sem_gather_dense (_fast.pyx:44-54)
+ *   srlu_fwht_rows            <- _kernels.fwht_rows (_fast.pyx:23-41)
+ *   srlu_sketch_left_dense    <- matrix.py:201-207 permute_rows +
+ *                                sketch.py:371-378 apply_sketch_left =
+ *                                _fast.pyx:71-78 sem_scatter_dense +
+ *                                sketch.py:338-349 _fast_mul_left (fused;
+ *                                P·A is never materialised)
+ *   srlu_sketch_left_csr      <- same with _fast.pyx:81-90 sem_scatter_csc
+ *   srlu_lu_rowpiv            <- factor.py:49-77 lu_row_pivot
+ *   srlu_lu_colpiv            <- factor.py:80-109 lu_col_pivot
+ */
+#ifndef SRLU_H
+#define SRLU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *srlu_stream_t; /* == cudaStream_t */
+
+#define SRLU_OK 0
+#define SRLU_ERR_ARG (-1)
+#define SRLU_ERR_CUDA (-2)
+#define SRLU_ERR_UNSUPPORTED (-3)
+#define SRLU_ERR_WORKSPACE (-4)
+
+/* element type codes of the input matrix A (arithmetic is always fp64) */
+#define SRLU_F32 0
+#define SRLU_F64 1
+
+const char *srlu_last_error(void);
+int srlu_version(void);
+
+/* ---- seed-derived draws (K0) ------------------------------------------ */
+
+/* numpy SeedSequence(seed).generate_state(2, uint64): the Philox key. Host. */
+int srlu_seed_key(uint64_t seed, uint64_t key[2]);
+
+/* build_fast_transform(k, l, "hadamard", seed) on the HOST (pad <= 2^20
+ * sequential Fisher-Yates swaps): phase[l] = +-1, sample_idx[k], *pad. */
+int srlu_draw_fast_transform(uint64_t seed, int64_t k, int64_t l, double *phase,
+                             int64_t *sample_idx, int64_t *pad);
+
+/* build_sem(l, n, seed) on the DEVICE: row_of[n] in [0,l), sign[n] = +-1.
+ * Bit-exact with numpy Generator(Philox(seed)).integers (Lemire). */
+size_t srlu_draw_sem_workspace(int64_t n, int64_t l);
+int srlu_draw_sem(uint64_t seed, int64_t l, int64_t n, int32_t *row_of, double *sign,
+                  void *ws, size_t ws_bytes, srlu_stream_t stream);
+
+/* ---- sparse-embedding plan -------------------------------------------- */
+
+/* Stable bucket sort of the n sources by row_of: sorted[bucket_ptr[t] ..
+ * bucket_ptr[t+1]) lists, ascending, the sources j with row_of[j] == t;
+ * the sign is folded into bit 31 (set = -1). */
+size_t srlu_sem_plan_workspace(int64_t n, int64_t l);
+int srlu_sem_plan(const int32_t *row_of, const double *sign, int64_t n, int64_t l,
+                  int32_t *sorted, int32_t *bucket_ptr, void *ws, size_t ws_bytes,
+                  srlu_stream_t stream);
+
+/* ---- stage 1: Y = A · Omega1^*  (K1) ----------------------------------- */
+
+/* A: m x n row-major (lda >= n), dtype SRLU_F32/F64.  Y: m x k1 row-major
+ * fp64.  mult1 = scale/sqrt(pad1).  *nonfinite |= 1 if any Y entry (hence
+ * any A entry) is not finite. */
+int srlu_sketch_right_dense(const void *a, int dtype, int64_t m, int64_t n, int64_t lda,
+                            const int32_t *sorted1, const int32_t *bucket_ptr1, int64_t l1,
+                            const double *phase1, const int32_t *idx1, int64_t k1,
+                            int64_t pad1, double mult1, double *y, int64_t ldy,
+                            int *nonfinite, srlu_stream_t stream);
+
+/* A in CSR: indptr[m+1] (int64), indices (int32, ascending per row),
+ * values (dtype).  row_of1/sign1: the raw draws. */
+int srlu_sketch_right_csr(const int64_t *indptr, const int32_t *indices, const void *vals,
+                          int dtype, int64_t m, int64_t n, const int32_t *row_of1,
+                          const double *sign1, int64_t l1, const double *phase1,
+                          const int32_t *idx1, int64_t k1, int64_t pad1, double mult1,
+                          double *y, int64_t ldy, int *nonfinite, srlu_stream_t stream);
+
+/* plugin seam: out (m x l row-major fp64) = A · S^T (no transform) */
+int srlu_sem_gather_dense(const void *a, int dtype, int64_t m, int64_t n, int64_t lda,
+                          const int32_t *sorted, const int32_t *bucket_ptr, int64_t l,
+                          double *out, int64_t ldo, srlu_stream_t stream);
+
+/* plugin seam: in-place unnormalised Walsh-Hadamard of each row of x
+ * (m x n row-major fp64, n a power of two, ldx >= n) */
+int srlu_fwht_rows(double *x, int64_t m, int64_t n, int64_t ldx, srlu_stream_t stream);
+
+/* ---- stage 2: Omega2 · (P A)  (K3) ------------------------------------- */
+
+/* Member table for the left sketch of P·A restricted to the local row
+ * shard [row0, row0+rows): for every PA index q (grouped by bucket via
+ * sorted2/bucket_ptr2), member_row[e] = perm[q]-row0 if that row is local,
+ * else -1; member_sign[e] = +-1.  perm == NULL means P = identity. */
+int srlu_sem_members(const int32_t *sorted2, int64_t m, const int64_t *perm, int64_t row0,
+                     int64_t rows, int32_t *member_row, double *member_sign,
+                     srlu_stream_t stream);
+
+/* out (n x k2 row-major, ldo >= k2) = (Omega2 · P A)^T over the local rows.
+ * S (l2 x n fp64) is caller scratch: srlu_sketch_left_workspace bytes. */
+size_t srlu_sketch_left_workspace(int64_t n, int64_t l2, int64_t pad2);
+int srlu_sketch_left_dense(const void *a, int dtype, int64_t rows, int64_t n, int64_t lda,
+                           const int32_t *member_row, const double *member_sign,
+                           const int32_t *bucket_ptr2, int64_t l2, const double *phase2,
+                           const int32_t *idx2, int64_t k2, int64_t pad2, double mult2,
+                           double *out, int64_t ldo, void *ws, size_t ws_bytes,
+                           srlu_stream_t stream);
+
+/* plugin seam: out (l x n row-major fp64, ldo >= n) = S · (P A) over the
+ * members (no transform); rows with member_row < 0 are skipped. */
+int srlu_sem_scatter_dense(const void *a, int dtype, int64_t rows, int64_t n, int64_t lda,
+                           const int32_t *member_row, const double *member_sign,
+                           const int32_t *bucket_ptr, int64_t l, double *out, int64_t ldo,
+                           srlu_stream_t stream);
+
+/* CSR variant; inv_perm[row] = PA index of local row (row0 offset applied
+ * by the caller), row_of2/sign2 indexed by PA index.  *flags |= 2 if a
+ * column holds more nonzeros than one CTA sorts in shared memory (8192). */
+size_t srlu_sketch_left_csr_workspace(int64_t rows, int64_t n, int64_t nnz, int64_t l2,
+                                      int64_t pad2);
+int srlu_sketch_left_csr(const int64_t *indptr, const int32_t *indices, const void *vals,
+                         int dtype, int64_t rows, int64_t n, int64_t nnz,
+                         const int32_t *inv_perm, const int32_t *row_of2, const double *sign2,
+                         int64_t l2, const double *phase2, const int32_t *idx2, int64_t k2,
+                         int64_t pad2, double mult2, double *out, int64_t ldo, void *ws,
+                         size_t ws_bytes, int *flags, srlu_stream_t stream);
+
+/* ---- pivoted LU of the sketches (K2, K5) ------------------------------- */
+
+/* Workspace for a persistent LU over M entities of k values. */
+size_t srlu_lu_workspace(int64_t M, int64_t k);
+
+/* Row-pivoted LU of Y (m x k row-major, overwritten as scratch):
+ * perm[m] (position -> row), L (m x k row-major, position order, unit
+ * lower-trapezoidal), U (k x k row-major, may be NULL). */
+int srlu_lu_rowpiv(double *y, int64_t m, int64_t k, int64_t ldy, int64_t *perm, double *L,
+                   int64_t ldl, double *U, int64_t ldu, void *ws, size_t ws_bytes,
+                   srlu_stream_t stream);
+
+/* Column-pivoted LU of core (k x n) given as its transpose ct (n x k
+ * row-major, overwritten): q[n], Lt (k x k row-major unit lower),
+ * UT (n x k row-major) = U^T, i.e. U (k x n) in column-major storage. */
+int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int64_t *q, double *Lt,
+                   int64_t ldlt, double *UT, int64_t ldut, void *ws, size_t ws_bytes,
+                   srlu_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRLU_H */

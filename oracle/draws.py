@@ -181,24 +181,23 @@ class Stream:
         if r == 1:
             return np.zeros(size, dtype=np.int64)
         thresh = ((1 << 32) - r) % r
-        # fast path: draw size words, redo the tail on any rejection
-        out = np.empty(size, dtype=np.int64)
-        done = 0
-        while done < size:
-            w = self.take(size - done).astype(np.uint64)
+        parts = []
+        need = size
+        while need > 0:
+            w = self.take(need + 64).astype(np.uint64)
             m = w * np.uint64(r)
             lo = m & _U32
-            bad = (lo < np.uint64(r)) & (lo < np.uint64(thresh))
-            if not bad.any():
-                out[done:] = (m >> _S32).astype(np.int64)
-                done = size
-                break
-            first = int(np.argmax(bad))
-            out[done:done + first] = (m[:first] >> _S32).astype(np.int64)
-            done += first
-            # rewind to just after the rejected word
-            self.pos -= (w.size - first - 1)
-        return out
+            ok = ~((lo < np.uint64(r)) & (lo < np.uint64(thresh)))
+            acc = np.flatnonzero(ok)
+            if acc.size >= need:
+                last = int(acc[need - 1])
+                parts.append((m[acc[:need]] >> _S32).astype(np.int64))
+                self.pos -= w.size - last - 1      # rewind past the last used word
+                need = 0
+            else:
+                parts.append((m[acc] >> _S32).astype(np.int64))
+                need -= acc.size
+        return np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
 
     def permutation(self, n: int) -> np.ndarray:
         """``Generator.permutation(n)``: Fisher-Yates from the top."""

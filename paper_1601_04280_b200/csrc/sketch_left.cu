@@ -1,0 +1,213 @@
+// K3 — stage-2 projection  Omega2 · (P A)  (reference: matrix.py:201-207
+// permute_rows + sketch.py:371-378 apply_sketch_left = _fast.pyx:71-78
+// sem_scatter_dense + sketch.py:338-349 _fast_mul_left).
+//
+// P·A is never materialised.  K3a: one CTA per (bucket t, column tile)
+// streams, in ascending PA index q, the member rows perm[q] of bucket t
+// (srlu_sem_members) straight from A and accumulates the signed rows in
+// registers -> S[t, cols] (exactly the reference's (bucket, column) order).
+// Every row of A is read exactly once.  K3b: one CTA per column group
+// applies +-phase, the radix-2 FWHT down the bucket axis (pad2) and the
+// k2-row subsample, writing (Omega2 P A)^T (n x k2).  Only the l2 x n
+// bucket matrix S (about 6% of A's bytes at the BASELINE configs) makes a
+// round trip, mostly through L2.
+#include "fwht.cuh"
+
+namespace srlu {
+
+template <typename T, int V, int NT>
+__global__ void __launch_bounds__(NT) k3a_dense_kernel(const T *__restrict__ a, int64_t rows,
+                                                       int64_t n, int64_t lda,
+                                                       const int32_t *__restrict__ member_row,
+                                                       const double *__restrict__ member_sign,
+                                                       const int32_t *__restrict__ bptr,
+                                                       double *__restrict__ S, int64_t lds) {
+    const int t = blockIdx.x;
+    const int64_t c0 = ((int64_t)blockIdx.y * NT + threadIdx.x) * V;
+    if (c0 >= n) return;
+    const bool full = c0 + V <= n;
+    double acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0.0;
+    const int beg = bptr[t], end = bptr[t + 1];
+    constexpr int U = 4;
+    int e = beg;
+    for (; e + U <= end; e += U) {
+        int r[U];
+        double sg[U];
+        T x[U][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            r[u] = __ldg(member_row + e + u);
+            sg[u] = __ldg(member_sign + e + u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (r[u] >= 0) {
+                const T *src = a + (int64_t)r[u] * lda + c0;
+                if constexpr (V == 1) {
+                    x[u][0] = __ldcs(src);
+                } else if (full) {
+                    if constexpr (sizeof(T) * V == 16) {
+                        if constexpr (sizeof(T) == 4) {
+                            float4 q = __ldcs(reinterpret_cast<const float4 *>(src));
+                            x[u][0] = q.x; x[u][1] = q.y; x[u][2] = q.z; x[u][3] = q.w;
+                        } else {
+                            double2 q = __ldcs(reinterpret_cast<const double2 *>(src));
+                            x[u][0] = q.x; x[u][1] = q.y;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) x[u][v] = c0 + v < n ? src[v] : T(0);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (r[u] >= 0) {
+                const bool neg = sg[u] < 0.0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    double d = (double)x[u][v];
+                    acc[v] = __dadd_rn(acc[v], neg ? -d : d);
+                }
+            }
+        }
+    }
+    for (; e < end; ++e) {
+        const int r = member_row[e];
+        if (r < 0) continue;
+        const bool neg = member_sign[e] < 0.0;
+        const T *src = a + (int64_t)r * lda + c0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (c0 + v < n) {
+                double d = (double)src[v];
+                acc[v] = __dadd_rn(acc[v], neg ? -d : d);
+            }
+        }
+    }
+    double *dst = S + (int64_t)t * lds + c0;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+        if (c0 + v < n) dst[v] = acc[v];
+}
+
+// one CTA per CB columns: x[t][c] = phase[t]*S[t][c]; FWHT over t; sample
+__global__ void k3b_kernel(const double *__restrict__ S, int64_t n, int l, int pad, int CB,
+                           const double *__restrict__ phase, const int32_t *__restrict__ idx,
+                           int k, double mult, double *__restrict__ out, int64_t ldo) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xs = reinterpret_cast<double *>(smem_raw);
+    const int64_t c0 = (int64_t)blockIdx.x * CB;
+    const int nc = (int)((n - c0) < CB ? (n - c0) : CB);
+    for (int w = threadIdx.x; w < pad * CB; w += blockDim.x) {
+        int t = w / CB, c = w % CB;
+        double v = 0.0;
+        if (t < l && c < nc) {
+            v = S[(int64_t)t * n + c0 + c];
+            if (phase[t] < 0.0) v = -v;
+        }
+        xs[w] = v;
+    }
+    __syncthreads();
+    fwht_smem_cols(xs, pad, CB, CB);
+    for (int w = threadIdx.x; w < nc * k; w += blockDim.x) {
+        int c = w / k, kk = w % k;
+        out[(c0 + c) * ldo + kk] = __dmul_rn(xs[idx[kk] * CB + c], mult);
+    }
+}
+
+template <typename T>
+static int launch_k3a(const T *a, int64_t rows, int64_t n, int64_t lda, const int32_t *member_row,
+                      const double *member_sign, const int32_t *bptr, int64_t l2, double *S,
+                      int64_t lds, cudaStream_t stream) {
+    constexpr int NT = 128;
+    constexpr int V = 16 / sizeof(T);
+    bool vec_ok = ((uintptr_t)a % 16 == 0) && (lda % V == 0);
+    if (vec_ok) {
+        dim3 grid((unsigned)l2, (unsigned)ceil_div(n, NT * V));
+        k3a_dense_kernel<T, V, NT><<<grid, NT, 0, stream>>>(a, rows, n, lda, member_row,
+                                                            member_sign, bptr, S, lds);
+    } else {
+        dim3 grid((unsigned)l2, (unsigned)ceil_div(n, NT));
+        k3a_dense_kernel<T, 1, NT><<<grid, NT, 0, stream>>>(a, rows, n, lda, member_row,
+                                                            member_sign, bptr, S, lds);
+    }
+    SRLU_CHECK_LAUNCH("k3a_dense_kernel");
+    return SRLU_OK;
+}
+
+int launch_k3b(const double *S, int64_t n, int64_t l2, int64_t pad2, const double *phase2,
+               const int32_t *idx2, int64_t k2, double mult2, double *out, int64_t ldo,
+               cudaStream_t stream) {
+    int CB = (int)(8192 / pad2);
+    if (CB < 1) CB = 1;
+    if (CB > 64) CB = 64;
+    size_t smem = (size_t)pad2 * CB * 8;
+    SRLU_REQUIRE(smem <= 200 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left: pad2=%lld too large",
+                 (long long)pad2);
+    SRLU_CUDA(cudaFuncSetAttribute(k3b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    k3b_kernel<<<(unsigned)ceil_div(n, CB), 256, smem, stream>>>(S, n, (int)l2, (int)pad2, CB,
+                                                                 phase2, idx2, (int)k2, mult2,
+                                                                 out, ldo);
+    SRLU_CHECK_LAUNCH("k3b_kernel");
+    return SRLU_OK;
+}
+
+}  // namespace srlu
+
+using namespace srlu;
+
+extern "C" size_t srlu_sketch_left_workspace(int64_t n, int64_t l2, int64_t pad2) {
+    (void)pad2;
+    return sizeof(double) * (size_t)(n * l2) + 256;
+}
+
+extern "C" int srlu_sketch_left_dense(const void *a, int dtype, int64_t rows, int64_t n,
+                                      int64_t lda, const int32_t *member_row,
+                                      const double *member_sign, const int32_t *bptr2, int64_t l2,
+                                      const double *phase2, const int32_t *idx2, int64_t k2,
+                                      int64_t pad2, double mult2, double *out, int64_t ldo,
+                                      void *ws, size_t ws_bytes, srlu_stream_t stream) {
+    SRLU_REQUIRE(rows >= 0 && n >= 1 && lda >= n && l2 >= 1 && k2 >= 1 && k2 <= pad2 &&
+                     pad2 >= l2 && (pad2 & (pad2 - 1)) == 0 && ldo >= k2,
+                 SRLU_ERR_ARG, "sketch_left_dense: bad sizes");
+    SRLU_REQUIRE(l2 < 65536, SRLU_ERR_UNSUPPORTED, "sketch_left_dense: l2 >= 65536");
+    SRLU_REQUIRE(ws_bytes >= srlu_sketch_left_workspace(n, l2, pad2), SRLU_ERR_WORKSPACE,
+                 "sketch_left_dense: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    double *S = (double *)ws;
+    int rc;
+    if (dtype == SRLU_F32)
+        rc = launch_k3a<float>((const float *)a, rows, n, lda, member_row, member_sign, bptr2, l2,
+                               S, n, s);
+    else if (dtype == SRLU_F64)
+        rc = launch_k3a<double>((const double *)a, rows, n, lda, member_row, member_sign, bptr2,
+                                l2, S, n, s);
+    else {
+        set_error("sketch_left_dense: unknown dtype %d", dtype);
+        return SRLU_ERR_ARG;
+    }
+    if (rc) return rc;
+    return launch_k3b(S, n, l2, pad2, phase2, idx2, k2, mult2, out, ldo, s);
+}
+
+extern "C" int srlu_sem_scatter_dense(const void *a, int dtype, int64_t rows, int64_t n,
+                                      int64_t lda, const int32_t *member_row,
+                                      const double *member_sign, const int32_t *bptr, int64_t l,
+                                      double *out, int64_t ldo, srlu_stream_t stream) {
+    SRLU_REQUIRE(rows >= 0 && n >= 1 && lda >= n && l >= 1 && ldo >= n, SRLU_ERR_ARG,
+                 "sem_scatter_dense: bad sizes");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == SRLU_F32)
+        return launch_k3a<float>((const float *)a, rows, n, lda, member_row, member_sign, bptr, l,
+                                 out, ldo, s);
+    if (dtype == SRLU_F64)
+        return launch_k3a<double>((const double *)a, rows, n, lda, member_row, member_sign, bptr,
+                                  l, out, ldo, s);
+    set_error("sem_scatter_dense: unknown dtype %d", dtype);
+    return SRLU_ERR_ARG;
+}

@@ -1,0 +1,250 @@
+// K3-CSR — stage-2 projection of a CSR matrix: Omega2 · (P A)
+// (reference: matrix.py:201-207 permute_rows of the CSC array +
+//  _fast.pyx:81-90 sem_scatter_csc + sketch.py:338-349 _fast_mul_left).
+//
+// The reference sums, for every (bucket t, column j), the signed entries
+// of P·A in ascending PA-row index q.  CSR rows of A are scattered into
+// per-column segments (counting sort by column; slot order inside a
+// column is arbitrary), each entry carrying the key (t = h2(q), q).  One
+// CTA per column then sorts its segment by key in shared memory (bitonic),
+// folds each bucket's run in ascending q (bit-identical sums), applies
+// +-phase, the radix-2 FWHT over pad2 and the k2-row subsample, and writes
+// row j of (Omega2 P A)^T.  P·A is never formed.
+#include "fwht.cuh"
+
+namespace srlu {
+
+constexpr int kCsrColCap = 8192;  // entries of one column sorted in smem
+
+__global__ void csr_col_count_kernel(const int32_t *__restrict__ indices, int64_t nnz,
+                                     int *__restrict__ cnt) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+         p += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + indices[p], 1);
+}
+
+// single CTA exclusive scan (int counts -> int64 pointers)
+__global__ void csr_col_scan_kernel(const int *__restrict__ cnt, int64_t n,
+                                    int64_t *__restrict__ colptr, int *__restrict__ maxcnt) {
+    __shared__ int64_t part[1024];
+    __shared__ int pmax[1024];
+    const int nt = blockDim.x;
+    const int64_t per = (n + nt - 1) / nt;
+    const int64_t lo = threadIdx.x * per, hi = min(n, lo + per);
+    int64_t s = 0;
+    int mx = 0;
+    for (int64_t j = lo; j < hi; ++j) {
+        s += cnt[j];
+        mx = max(mx, cnt[j]);
+    }
+    part[threadIdx.x] = s;
+    pmax[threadIdx.x] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        int m2 = 0;
+        for (int i = 0; i < nt; ++i) {
+            int64_t c = part[i];
+            part[i] = run;
+            run += c;
+            m2 = max(m2, pmax[i]);
+        }
+        colptr[n] = run;
+        *maxcnt = m2;
+    }
+    __syncthreads();
+    int64_t run = part[threadIdx.x];
+    for (int64_t j = lo; j < hi; ++j) {
+        colptr[j] = run;
+        run += cnt[j];
+    }
+}
+
+template <typename T>
+__global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
+                                const int32_t *__restrict__ indices, const T *__restrict__ vals,
+                                int64_t rows, const int32_t *__restrict__ inv_perm,
+                                const int32_t *__restrict__ row_of2,
+                                const double *__restrict__ sign2,
+                                const int64_t *__restrict__ colptr, int *__restrict__ fill,
+                                unsigned long long *__restrict__ keys, double *__restrict__ ev) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < rows; r += nwarp) {
+        const int q = inv_perm[r];
+        const unsigned long long key =
+            ((unsigned long long)(unsigned)row_of2[q] << 32) | (unsigned)q;
+        const bool neg = sign2[q] < 0.0;
+        for (int64_t p = indptr[r] + lane; p < indptr[r + 1]; p += 32) {
+            const int j = indices[p];
+            const int64_t slot = colptr[j] + atomicAdd(fill + j, 1);
+            const double v = (double)vals[p];
+            keys[slot] = key;
+            ev[slot] = neg ? -v : v;
+        }
+    }
+}
+
+__global__ void csr_col_project_kernel(const int64_t *__restrict__ colptr,
+                                       const unsigned long long *__restrict__ keys,
+                                       const double *__restrict__ ev, int64_t n, int l, int pad,
+                                       const double *__restrict__ phase,
+                                       const int32_t *__restrict__ idx, int k, double mult,
+                                       double *__restrict__ out, int64_t ldo, int *flags) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *x = reinterpret_cast<double *>(smem_raw);                    // pad
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(x + pad);  // cap
+    double *sv = reinterpret_cast<double *>(sk + kCsrColCap);            // cap
+    for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+        const int64_t p0 = colptr[j];
+        const int cnt = (int)(colptr[j + 1] - p0);
+        for (int t = threadIdx.x; t < pad; t += blockDim.x) x[t] = 0.0;
+        if (cnt > kCsrColCap) {
+            if (threadIdx.x == 0) atomicOr(flags, 2);
+            __syncthreads();
+            continue;
+        }
+        int n2 = 1;
+        while (n2 < cnt) n2 <<= 1;
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+            if (i < cnt) {
+                sk[i] = keys[p0 + i];
+                sv[i] = ev[p0 + i];
+            } else {
+                sk[i] = ~0ULL;
+                sv[i] = 0.0;
+            }
+        }
+        __syncthreads();
+        for (int kk = 2; kk <= n2; kk <<= 1) {
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                    const int ixj = i ^ jj;
+                    if (ixj > i) {
+                        const bool up = (i & kk) == 0;
+                        unsigned long long a = sk[i], b = sk[ixj];
+                        if ((a > b) == up) {
+                            sk[i] = b;
+                            sk[ixj] = a;
+                            double tv = sv[i];
+                            sv[i] = sv[ixj];
+                            sv[ixj] = tv;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // fold each bucket's run in ascending q (reference order)
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const unsigned t = (unsigned)(sk[i] >> 32);
+            if (i > 0 && (unsigned)(sk[i - 1] >> 32) == t) continue;
+            double acc = 0.0;
+            for (int e = i; e < cnt && (unsigned)(sk[e] >> 32) == t; ++e) acc = __dadd_rn(acc, sv[e]);
+            x[t] = phase[t] < 0.0 ? -acc : acc;
+        }
+        __syncthreads();
+        fwht_smem_cta(x, pad);
+        for (int kk = threadIdx.x; kk < k; kk += blockDim.x)
+            out[j * ldo + kk] = __dmul_rn(x[idx[kk]], mult);
+        __syncthreads();
+    }
+}
+
+struct CsrWs {
+    int *cnt, *fill, *maxcnt;
+    int64_t *colptr;
+    unsigned long long *keys;
+    double *ev;
+};
+
+static size_t csr_ws_layout(int64_t n, int64_t nnz, char *base, CsrWs *w) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return base ? base + o : nullptr;
+    };
+    char *p;
+    p = take(sizeof(int) * n);             if (w) w->cnt = (int *)p;
+    p = take(sizeof(int) * n);             if (w) w->fill = (int *)p;
+    p = take(sizeof(int) * 4);             if (w) w->maxcnt = (int *)p;
+    p = take(sizeof(int64_t) * (n + 1));   if (w) w->colptr = (int64_t *)p;
+    p = take(sizeof(unsigned long long) * (nnz > 0 ? nnz : 1)); if (w) w->keys = (unsigned long long *)p;
+    p = take(sizeof(double) * (nnz > 0 ? nnz : 1));             if (w) w->ev = (double *)p;
+    return off;
+}
+
+template <typename T>
+static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *vals, int64_t rows,
+                        int64_t n, int64_t nnz, const int32_t *inv_perm, const int32_t *row_of2,
+                        const double *sign2, int64_t l2, const double *phase2,
+                        const int32_t *idx2, int64_t k2, int64_t pad2, double mult2,
+                        double *out, int64_t ldo, void *ws, int *flags, cudaStream_t s) {
+    CsrWs w;
+    csr_ws_layout(n, nnz, (char *)ws, &w);
+    SRLU_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int) * n, s));
+    SRLU_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int) * n, s));
+    if (nnz > 0) {
+        csr_col_count_kernel<<<148 * 8, 256, 0, s>>>(indices, nnz, w.cnt);
+        SRLU_CHECK_LAUNCH("csr_col_count_kernel");
+    }
+    csr_col_scan_kernel<<<1, 1024, 0, s>>>(w.cnt, n, w.colptr, w.maxcnt);
+    SRLU_CHECK_LAUNCH("csr_col_scan_kernel");
+    if (rows > 0) {
+        int64_t blocks = ceil_div(rows * 32, 256);
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        csr_fill_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(indptr, indices, vals, rows, inv_perm,
+                                                           row_of2, sign2, w.colptr, w.fill,
+                                                           w.keys, w.ev);
+        SRLU_CHECK_LAUNCH("csr_fill_kernel");
+    }
+    size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * kCsrColCap;
+    SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left_csr: pad2 too large");
+    SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int64_t grid = n < 148 * 8 ? n : 148 * 8;
+    csr_col_project_kernel<<<(unsigned)grid, 256, smem, s>>>(w.colptr, w.keys, w.ev, n, (int)l2,
+                                                             (int)pad2, phase2, idx2, (int)k2,
+                                                             mult2, out, ldo, flags);
+    SRLU_CHECK_LAUNCH("csr_col_project_kernel");
+    return SRLU_OK;
+}
+
+}  // namespace srlu
+
+using namespace srlu;
+
+extern "C" size_t srlu_sketch_left_csr_workspace(int64_t rows, int64_t n, int64_t nnz, int64_t l2,
+                                                 int64_t pad2) {
+    (void)rows; (void)l2; (void)pad2;
+    return csr_ws_layout(n, nnz, nullptr, nullptr) + 256;
+}
+
+extern "C" int srlu_sketch_left_csr(const int64_t *indptr, const int32_t *indices,
+                                    const void *vals, int dtype, int64_t rows, int64_t n,
+                                    int64_t nnz, const int32_t *inv_perm, const int32_t *row_of2,
+                                    const double *sign2, int64_t l2, const double *phase2,
+                                    const int32_t *idx2, int64_t k2, int64_t pad2, double mult2,
+                                    double *out, int64_t ldo, void *ws, size_t ws_bytes,
+                                    int *flags, srlu_stream_t stream) {
+    SRLU_REQUIRE(rows >= 0 && n >= 1 && l2 >= 1 && k2 >= 1 && k2 <= pad2 && pad2 >= l2 &&
+                     (pad2 & (pad2 - 1)) == 0 && ldo >= k2 && nnz >= 0,
+                 SRLU_ERR_ARG, "sketch_left_csr: bad sizes");
+    SRLU_REQUIRE(rows < (1LL << 31) && l2 < (1LL << 31), SRLU_ERR_UNSUPPORTED,
+                 "sketch_left_csr: sizes beyond int32");
+    SRLU_REQUIRE(ws_bytes >= srlu_sketch_left_csr_workspace(rows, n, nnz, l2, pad2),
+                 SRLU_ERR_WORKSPACE, "sketch_left_csr: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == SRLU_F32)
+        return run_csr_left<float>(indptr, indices, (const float *)vals, rows, n, nnz, inv_perm,
+                                   row_of2, sign2, l2, phase2, idx2, k2, pad2, mult2, out, ldo,
+                                   ws, flags, s);
+    if (dtype == SRLU_F64)
+        return run_csr_left<double>(indptr, indices, (const double *)vals, rows, n, nnz,
+                                    inv_perm, row_of2, sign2, l2, phase2, idx2, k2, pad2, mult2,
+                                    out, ldo, ws, flags, s);
+    set_error("sketch_left_csr: unknown dtype %d", dtype);
+    return SRLU_ERR_ARG;
+}

@@ -1,0 +1,135 @@
+"""Pivoted LUs and the left pseudo-inverse on the device (factor.py).
+
+``lu_row_pivot`` / ``lu_col_pivot`` run the persistent CUDA kernel K2/K5
+(bit-exact replays of factor.py:49-77 / :80-109).  ``left_pseudo_inverse``
+keeps the reference's Householder-QR formulation and sigma-ratio rank test
+(factor.py:112-130); in this round it runs on cuSOLVER through torch.linalg
+(a ≤ 558 x 550 problem, <1% of the step) — see DESIGN.md §5.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import ShapeError, SingularMatrixError
+from .matrix import Matrix, Permutation
+
+PIVOT_RTOL = 1e-14   # factor.py:19 (compiled into lu.cu)
+RANK_RTOL = 1e-10    # factor.py:22
+
+
+class PivotedLU:
+    """P B = L U, unit lower-trapezoidal L, square upper U (factor.py:25-34)."""
+
+    __slots__ = ("P", "L", "U")
+
+    def __init__(self, P, L, U):
+        self.P, self.L, self.U = P, L, U
+
+
+class ColPivotedLU:
+    """M Q = L U, unit lower L, upper-trapezoidal U (factor.py:37-46)."""
+
+    __slots__ = ("Q", "L", "U")
+
+    def __init__(self, Q, L, U):
+        self.Q, self.L, self.U = Q, L, U
+
+
+def lu_row_pivot_dev(y: torch.Tensor, want_u: bool = False, stream=None):
+    """K2 on a row-major fp64 m x k device tensor (overwritten).
+    Returns (perm int64[m] device, L m x k, U k x k or None)."""
+    L = _lib.lib()
+    m, k = y.shape
+    if m < k:
+        raise ShapeError(f"need rows >= cols, got {m} x {k}")
+    dev = y.device
+    perm = torch.empty(m, dtype=torch.int64, device=dev)
+    lo = torch.empty(m, k, dtype=torch.float64, device=dev)
+    up = torch.zeros(k, k, dtype=torch.float64, device=dev) if want_u else None
+    ws = _lib.workspace(L.srlu_lu_workspace(m, k), dev)
+    _lib.check(L.srlu_lu_rowpiv(_lib.ptr(y), m, k, y.stride(0), _lib.ptr(perm), _lib.ptr(lo),
+                                lo.stride(0), _lib.ptr(up), k, _lib.ptr(ws), ws.numel(),
+                                _lib.stream_handle(stream)), "lu_row_pivot")
+    return perm, lo, up
+
+
+def lu_col_pivot_dev(ct: torch.Tensor, stream=None):
+    """K5 on core^T (n x k row-major fp64 device tensor, overwritten).
+    Returns (q int64[n], Lt k x k, UT n x k) with U = UT^T."""
+    L = _lib.lib()
+    n, k = ct.shape
+    if k > n:
+        raise ShapeError(f"need rows <= cols, got {k} x {n}")
+    dev = ct.device
+    q = torch.empty(n, dtype=torch.int64, device=dev)
+    lt = torch.zeros(k, k, dtype=torch.float64, device=dev)
+    ut = torch.empty(n, k, dtype=torch.float64, device=dev)
+    ws = _lib.workspace(L.srlu_lu_workspace(n, k), dev)
+    _lib.check(L.srlu_lu_colpiv(_lib.ptr(ct), n, k, ct.stride(0), _lib.ptr(q), _lib.ptr(lt),
+                                lt.stride(0), _lib.ptr(ut), ut.stride(0), _lib.ptr(ws),
+                                ws.numel(), _lib.stream_handle(stream)), "lu_col_pivot")
+    return q, lt, ut
+
+
+def _dense_f64(b) -> torch.Tensor:
+    if isinstance(b, Matrix):
+        t = b.to_dense()
+    elif isinstance(b, torch.Tensor):
+        t = b
+    else:
+        t = Matrix(b).to_dense()
+    if not t.is_cuda:
+        t = t.cuda()
+    return t.to(torch.float64).contiguous().clone()
+
+
+def lu_row_pivot(b) -> PivotedLU:
+    """factor.py:49-77 on the device."""
+    y = _dense_f64(b)
+    if y.shape[0] < y.shape[1]:
+        raise ShapeError(f"need rows >= cols, got {y.shape[0]} x {y.shape[1]}")
+    perm, lo, up = lu_row_pivot_dev(y, want_u=True)
+    return PivotedLU(Permutation(perm.cpu().numpy(), perm), Matrix.from_device(lo),
+                     Matrix.from_device(up))
+
+
+def lu_col_pivot(mat) -> ColPivotedLU:
+    """factor.py:80-109 on the device."""
+    c = _dense_f64(mat)
+    k, n = c.shape
+    if k > n:
+        raise ShapeError(f"need rows <= cols, got {k} x {n}")
+    q, lt, ut = lu_col_pivot_dev(c.t().contiguous())
+    return ColPivotedLU(Permutation(q.cpu().numpy(), q), Matrix.from_device(lt),
+                        Matrix.from_device(ut.t().contiguous()))
+
+
+def pinv_dev(mat: torch.Tensor):
+    """Householder QR + sigma-ratio test + triangular solve on the device.
+    Returns (pinv k1 x k2, cond) with cond = sv_max / sv_min (a device
+    scalar); the caller decides singularity (one host sync)."""
+    qf, rf = torch.linalg.qr(mat, mode="reduced")
+    sv = torch.linalg.svdvals(rf)
+    pinv = torch.linalg.solve_triangular(rf, qf.t().contiguous(), upper=True)
+    return pinv, sv
+
+
+def check_rank(sv_host):
+    """factor.py:123-128"""
+    if sv_host[0] == 0.0 or sv_host[-1] <= RANK_RTOL * sv_host[0]:
+        cond = float("inf") if sv_host[-1] == 0.0 else float(sv_host[0] / sv_host[-1])
+        raise SingularMatrixError(
+            f"matrix is numerically rank deficient (condition estimate {cond:.3e})", cond=cond)
+
+
+def left_pseudo_inverse(mat) -> Matrix:
+    """factor.py:112-130 on the device."""
+    m = _dense_f64(mat)
+    p, q = m.shape
+    if p < q:
+        raise ShapeError(f"need rows >= cols, got {p} x {q}")
+    pinv, sv = pinv_dev(m)
+    check_rank(sv.cpu().numpy())
+    return Matrix.from_device(pinv)

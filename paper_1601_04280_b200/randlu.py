@@ -1,0 +1,302 @@
+"""Randomized low-rank pivoted LU on B200 — the drop-in for the reference's
+``sparse_randomized_lu`` (randlu.py:208-276).
+
+Same signature, parameter dataclass, result dataclass, error types,
+resample semantics (attempt t draws from sub-seeds seed+2t / seed+2t+1,
+up to MAX_RESAMPLES retries, warnings on the module logger) and the same
+``elapsed`` keys; every stage runs on the GPU:
+
+  sketch1  K0 draws + K1 fused CountSketch/FWHT stream over A  -> Y
+  lu1      K2 persistent row-pivoted LU of Y                   -> P, L1
+  sketch2  K3 fused left sketch of L1 and of P·A (P·A never materialised)
+  pinv     Householder QR + rank test + core = pinv · (Omega2 P A)
+  lu2      K5 persistent column-pivoted LU of core; L = L1 · L~
+
+Stage times come from CUDA events on the launching stream; the host
+synchronises once per attempt (rank test + non-finite flag).
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from .errors import DecompositionError, ParameterError, ShapeError, SingularMatrixError
+from .factor import RANK_RTOL, check_rank, lu_col_pivot_dev, lu_row_pivot_dev, pinv_dev
+from .matrix import COMPLEX, REAL, Matrix, Permutation
+from .sketch import (HADAMARD, build_composite, members, sketch_left_into, sketch_right_into,
+                     transform_kind_for_field)
+
+logger = logging.getLogger(__name__)
+
+MAX_RESAMPLES = 3        # randlu.py:46
+STAGES = ("sketch1", "lu1", "sketch2", "pinv", "lu2")
+
+
+@dataclass(frozen=True)
+class RandLuParams:
+    """randlu.py:49-95 (identical fields, defaults and invariants)."""
+
+    r: int
+    k1: int
+    l1: int
+    k2: int
+    l2: int
+    epsilon: float = 0.5
+    delta: float = 0.1
+    seed: int = 0
+    field: str = REAL
+
+    def __post_init__(self):
+        if self.r < 1:
+            raise ParameterError("target rank must be positive")
+        if not self.r <= self.k1 <= self.k2:
+            raise ParameterError(
+                f"need r <= k1 <= k2, got r={self.r}, k1={self.k1}, k2={self.k2}")
+        if not self.k1 < self.l1:
+            raise ParameterError(f"need k1 < l1, got k1={self.k1}, l1={self.l1}")
+        if not self.k2 < self.l2:
+            raise ParameterError(f"need k2 < l2, got k2={self.k2}, l2={self.l2}")
+        if not 0.0 < self.epsilon < 1.0:
+            raise ParameterError("epsilon must lie in (0, 1)")
+        if not 0.0 < self.delta < 1.0:
+            raise ParameterError("delta must lie in (0, 1)")
+        if self.field not in (REAL, COMPLEX):
+            raise ParameterError(f"unknown field {self.field!r}")
+
+    def check_against(self, m, n):
+        if self.l1 > n:
+            raise ParameterError(f"l1={self.l1} exceeds column count {n}")
+        if self.l2 > m:
+            raise ParameterError(f"l2={self.l2} exceeds row count {m}")
+        if self.k2 > m:
+            raise ParameterError(f"k2={self.k2} exceeds row count {m}")
+        if self.k1 > m:
+            raise ParameterError(f"k1={self.k1} exceeds row count {m}")
+
+
+@dataclass
+class RandLuResult:
+    """randlu.py:98-114.  P, Q: host Permutations (device copies cached);
+    L (m x k1), U (k1 x n): device Matrices.  ``elapsed`` in seconds."""
+
+    P: Permutation
+    Q: Permutation
+    L: Matrix
+    U: Matrix
+    elapsed: dict = dc_field(default_factory=dict)
+    attempt: int = 0
+    extras: dict = dc_field(default_factory=dict)
+
+
+def default_params(r, m, n, field=REAL, seed=0, mode="practical", epsilon=0.5,
+                   delta=0.1) -> RandLuParams:
+    """randlu.py:117-166 (practical and theoretical modes)."""
+    if not 0.0 < epsilon < 1.0:
+        raise ParameterError("epsilon must lie in (0, 1)")
+    if not 0.0 < delta < 1.0:
+        raise ParameterError("delta must lie in (0, 1)")
+    if mode == "practical":
+        if not 1 <= r <= min(m, n) / 2:
+            raise ParameterError(f"need 1 <= r <= min(m,n)/2, got r={r} for {m} x {n}")
+        k1 = min(n - 1, r + 8)
+        k2 = min(m - 1, k1 + 8)
+        l1 = min(n, 4 * k1)
+        l2 = min(m, 4 * k2)
+        if not r <= k1 < k2:
+            raise ParameterError(
+                f"degenerate size: clamped defaults collide (r={r}, k1={k1}, k2={k2} for {m} x {n})")
+    elif mode == "theoretical":
+        if not 1 <= r <= min(m, n):
+            raise ParameterError(f"need 1 <= r <= min(m,n), got r={r}")
+        re = r / epsilon
+        k1 = max(r + 1, math.ceil(re * math.log(max(re, 2.0))))
+        l1 = max(k1 + 1, math.ceil(r * r * math.log(max(re, 2.0)) ** 6 + re))
+        l2 = math.ceil((r * r + r) / ((2 * epsilon - epsilon ** 2) ** 2 * delta))
+        k2 = math.ceil(4.0 * (math.sqrt(r) + math.sqrt(8.0 * math.log(r * l2))) ** 2
+                       * math.log(max(r, 2.0)))
+        l1 = min(l1, n)
+        l2 = min(l2, m)
+        k1 = min(k1, l1 - 1, m)
+        k2 = min(max(k2, k1), l2 - 1, m - 1)
+        if not (r <= k1 <= k2 and k1 < l1 and k2 < l2):
+            raise ParameterError(f"theoretical sizes do not fit a {m} x {n} matrix at r={r}")
+    else:
+        raise ParameterError(f"unknown mode {mode!r}")
+    return RandLuParams(r=int(r), k1=int(k1), l1=int(l1), k2=int(k2), l2=int(l2),
+                        epsilon=epsilon, delta=delta, seed=int(seed), field=field)
+
+
+def params_from_north_star(m, n, k, l, width, seed=0) -> RandLuParams:
+    """The (A, k, l, seed) form of BASELINE.json: r = k, k1 = l, l1 = width,
+    k2 = min(m-1, k1+8), l2 = min(m, 4 k2) (the reference's practical rule,
+    randlu.py:136-139) — SURVEY.md §0 finding 3."""
+    k2 = min(m - 1, l + 8)
+    return RandLuParams(r=k, k1=l, l1=width, k2=k2, l2=min(m, 4 * k2), seed=seed)
+
+
+class _CompositeOps:
+    """Structured sketch pair for one attempt (randlu.py:169-181)."""
+
+    def __init__(self, params, m, n, seed1, seed2, device):
+        kind = transform_kind_for_field(params.field)
+        self.omega1 = build_composite(params.k1, params.l1, n, kind, seed1, device)
+        self.omega2 = build_composite(params.k2, params.l2, m, kind, seed2, device)
+
+
+def sparse_randomized_lu(a, params: RandLuParams, *, keep: bool = False) -> RandLuResult:
+    """Randomized pivoted LU with structured projections (randlu.py:208-213).
+    ``a``: Matrix, CUDA tensor (row-major fp32/fp64), numpy array or scipy
+    sparse.  Deterministic: same inputs and params give bit-identical
+    factors."""
+    if not isinstance(a, Matrix):
+        a = Matrix.from_device(a) if isinstance(a, torch.Tensor) and a.is_cuda else Matrix(a)
+    return _pipeline(a, params, keep)
+
+
+def gaussian_randomized_lu(a, params):  # randlu.py:216-219
+    raise NotImplementedError("the dense-Gaussian baseline is out of scope of the B200 path "
+                              "(SURVEY.md §2.1 row 9)")
+
+
+def _pipeline(a: Matrix, params: RandLuParams, keep: bool) -> RandLuResult:
+    m, n = a.shape
+    params.check_against(m, n)
+    if a.field != params.field:
+        raise ParameterError(f"params.field={params.field} but matrix field is {a.field}")
+    if params.field != REAL:
+        raise NotImplementedError("complex128 field is out of scope of the B200 path")
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    last = None
+    for attempt in range(1 + MAX_RESAMPLES):
+        try:
+            res = _attempt(a, params, attempt, keep)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t1.record()
+            t1.synchronize()
+            res.elapsed["total"] = t0.elapsed_time(t1) / 1e3
+            return res
+        except SingularMatrixError as err:
+            last = err
+            logger.warning("rank-deficient reduced system (attempt %d/%d, cond %.3e); "
+                           "resampling sketches", attempt + 1, 1 + MAX_RESAMPLES, err.cond)
+    raise DecompositionError(
+        f"reduced system stayed rank deficient after {MAX_RESAMPLES} resamples "
+        f"(last condition estimate {last.cond:.3e}); the sketch sizes "
+        f"k2={params.k2}, l2={params.l2} are likely too small") from last
+
+
+def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandLuResult:
+    m, n = a.shape
+    dev = a.device
+    k1, k2 = params.k1, params.k2
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
+    ev[0].record()
+    ops = _CompositeOps(params, m, n, params.seed + 2 * attempt, params.seed + 2 * attempt + 1,
+                        dev)
+    om1, om2 = ops.omega1, ops.omega2
+    y = torch.empty(m, k1, dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    sketch_right_into(a, om1, y, flag)
+    ev[1].record()
+
+    y_keep = y.clone() if keep else None
+    perm, l1, _ = lu_row_pivot_dev(y)
+    ev[2].record()
+
+    # stage 2: Omega2 L1 and Omega2 (P A)
+    mrow_l, msign_l, bptr2 = members(om2, None, 0, m)
+    red_lT = torch.empty(k1, k2, dtype=torch.float64, device=dev)
+    sketch_left_into(Matrix.from_device(l1), om2, mrow_l, msign_l, bptr2, red_lT)
+    red_aT = torch.empty(n, k2, dtype=torch.float64, device=dev)
+    if a.is_sparse:
+        inv = torch.empty(m, dtype=torch.int32, device=dev)
+        inv[perm] = torch.arange(m, dtype=torch.int32, device=dev)
+        sketch_left_into(a, om2, None, None, None, red_aT, inv_perm=inv, flags=flag)
+    else:
+        mrow, msign, _ = members(om2, perm, 0, m)
+        sketch_left_into(a, om2, mrow, msign, bptr2, red_aT)
+    ev[3].record()
+
+    pinv, sv = pinv_dev(red_lT.t())
+    core_t = red_aT @ pinv.t()          # (Omega2 P A)^T pinv^T = core^T, n x k1
+    ev[4].record()
+    core_keep = core_t.clone() if keep else None
+
+    q, lt, ut = lu_col_pivot_dev(core_t)
+    l_final = l1 @ lt
+    ev[5].record()
+
+    # the one host sync of the attempt: rank test + non-finite flag
+    sv_host = sv.cpu().numpy()
+    fl = int(flag.item())
+    if fl & 1:
+        raise ValueError("matrix entries must be finite")
+    if fl & 2:
+        raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
+    check_rank(sv_host)
+    elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
+    res = RandLuResult(P=Permutation(perm.cpu().numpy(), perm, validate=False),
+                       Q=Permutation(q.cpu().numpy(), q, validate=False),
+                       L=Matrix.from_device(l_final), U=_wrap(ut.t()), elapsed=elapsed,
+                       attempt=attempt)
+    if keep:
+        res.extras = dict(Y=y_keep, L1=l1, red_l=red_lT.t(), red_a=red_aT.t(), pinv=pinv,
+                          core=core_keep.t(), Lt=lt, omega1=om1, omega2=om2)
+    return res
+
+
+def _wrap(t: torch.Tensor) -> Matrix:
+    """Wrap a (possibly column-major) device tensor as a Matrix without a copy."""
+    mm = object.__new__(Matrix)
+    mm._dense = t
+    mm._indptr = mm._indices = mm._values = None
+    mm.rows, mm.cols = int(t.shape[0]), int(t.shape[1])
+    return mm
+
+
+def approximation_error(a, res: RandLuResult, block_cols: int = 4096) -> float:
+    """||L U - P A Q||_F (randlu.py:279-302) on the device, column blocks.
+    Evaluation only (never timed)."""
+    if not isinstance(a, Matrix):
+        a = Matrix.from_device(a) if isinstance(a, torch.Tensor) and a.is_cuda else Matrix(a)
+    m, n = a.shape
+    if res.L.rows != m or res.U.cols != n or res.L.cols != res.U.rows \
+            or res.P.size != m or res.Q.size != n:
+        raise ShapeError(f"factors {res.L.shape} x {res.U.shape} do not match target {a.shape}")
+    dev = a.device
+    perm = res.P.device_indices(dev)
+    cols = res.Q.device_indices(dev)
+    ld = res.L.to_dense().to(torch.float64)
+    ud = res.U.to_dense().to(torch.float64)
+    acc = torch.zeros((), dtype=torch.float64, device=dev)
+    if a.is_sparse:
+        indptr, indices, vals = a.raw
+        rows = torch.repeat_interleave(torch.arange(m, device=dev), indptr.diff())
+        inv_perm = torch.empty_like(perm)
+        inv_perm[perm] = torch.arange(m, device=dev)
+        inv_q = torch.empty_like(cols)
+        inv_q[cols] = torch.arange(n, device=dev)
+        prow = inv_perm[rows]
+        pcol = inv_q[indices.long()]
+        for start in range(0, n, block_cols):
+            stop = min(n, start + block_cols)
+            blk = ld @ ud[:, start:stop]
+            sel = (pcol >= start) & (pcol < stop)
+            blk.index_put_((prow[sel], pcol[sel] - start), -vals[sel].to(torch.float64),
+                           accumulate=True)
+            acc += (blk * blk).sum()
+    else:
+        t = a.raw
+        for start in range(0, n, block_cols):
+            stop = min(n, start + block_cols)
+            blk = ld @ ud[:, start:stop]
+            ref = t.index_select(1, cols[start:stop]).index_select(0, perm).to(torch.float64)
+            blk -= ref
+            acc += (blk * blk).sum()
+    return math.sqrt(float(acc))

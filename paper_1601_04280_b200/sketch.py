@@ -1,0 +1,300 @@
+"""Random projection operators on the device (the reference's sketch.py).
+
+Draws (K0) are bit-exact with the reference's numpy ``Generator(Philox)``
+streams (sketch.py:42-43, :103-114, :214-235, :269-278): the sparse
+embedding's n bucket/sign draws are generated on the GPU, the transform
+stage's l phases + Fisher-Yates permutation of ``pad`` items on the host
+(C, inside libsrlu).  Application runs the fused CUDA kernels K1 (right
+sketch, stage 1) and K3 (left sketch, stage 2).  Only the real64 /
+Walsh-Hadamard field is on the B200 path (every BASELINE config is real).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ParameterError, ShapeError
+from .matrix import COMPLEX, REAL, Matrix, _default_device
+
+STAGE_SEED_OFFSET = 1 << 32      # sketch.py:36
+FOURIER = "fourier"
+HADAMARD = "hadamard"
+
+
+def _next_pow2(n):
+    return 1 << (int(n) - 1).bit_length()
+
+
+def transform_kind_for_field(field):
+    """sketch.py:50-57"""
+    if field == REAL:
+        return HADAMARD
+    if field == COMPLEX:
+        return FOURIER
+    raise ParameterError(f"unknown field {field!r}")
+
+
+def _check_seed(seed):
+    seed = int(seed)
+    if seed < 0 or seed >= 1 << 64:
+        raise ParameterError(f"seed must lie in [0, 2**64), got {seed}")
+    return seed
+
+
+@dataclass(frozen=True, eq=False)
+class SparseEmbedding:
+    """k x n sparse sign embedding (sketch.py:60-100): column j has the
+    single entry sign[j] in row row_of[j].  Device arrays; the bucket-sorted
+    plan (sorted sources, bucket pointers) is built once, lazily."""
+
+    out_dim: int
+    in_dim: int
+    row_of: torch.Tensor   # int32 [in_dim]
+    sign: torch.Tensor     # float64 [in_dim], +-1
+    seed: int = 0
+    _plan: list = dc_field(default_factory=list, repr=False)
+
+    @property
+    def shape(self):
+        return (self.out_dim, self.in_dim)
+
+    def plan(self):
+        """(sorted int32[n] with sign in bit 31, bucket_ptr int32[l+1])."""
+        if not self._plan:
+            L = _lib.lib()
+            dev = self.row_of.device
+            srt = torch.empty(self.in_dim, dtype=torch.int32, device=dev)
+            bptr = torch.empty(self.out_dim + 1, dtype=torch.int32, device=dev)
+            ws = _lib.workspace(L.srlu_sem_plan_workspace(self.in_dim, self.out_dim), dev)
+            _lib.check(L.srlu_sem_plan(_lib.ptr(self.row_of), _lib.ptr(self.sign), self.in_dim,
+                                       self.out_dim, _lib.ptr(srt), _lib.ptr(bptr),
+                                       _lib.ptr(ws), ws.numel(), _lib.stream_handle()),
+                       "sem_plan")
+            self._plan.extend([srt, bptr])
+        return self._plan[0], self._plan[1]
+
+    def row_counts(self):
+        return torch.bincount(self.row_of.long(), minlength=self.out_dim)
+
+
+def build_sem(k, n, seed, device=None) -> SparseEmbedding:
+    """Draw a k x n sparse sign embedding on the device (sketch.py:103-114)."""
+    if not 1 <= k <= n:
+        raise ParameterError(f"need 1 <= k <= n, got k={k}, n={n}")
+    seed = _check_seed(seed)
+    L = _lib.lib()
+    dev = torch.device(device) if device is not None else _default_device()
+    row_of = torch.empty(n, dtype=torch.int32, device=dev)
+    sign = torch.empty(n, dtype=torch.float64, device=dev)
+    ws = _lib.workspace(L.srlu_draw_sem_workspace(n, k), dev)
+    _lib.check(L.srlu_draw_sem(seed, k, n, _lib.ptr(row_of), _lib.ptr(sign), _lib.ptr(ws),
+                               ws.numel(), _lib.stream_handle()), "build_sem")
+    return SparseEmbedding(int(k), int(n), row_of, sign, seed=seed)
+
+
+@dataclass(frozen=True, eq=False)
+class FastTransformSketch:
+    """k x l subsampled Walsh-Hadamard transform (sketch.py:143-201):
+    scale * Sample(H_pad/sqrt(pad) · diag(phase) x)."""
+
+    out_dim: int
+    in_dim: int
+    phase: torch.Tensor        # float64 [in_dim], +-1 (device)
+    sample_idx: torch.Tensor   # int32 [out_dim] (device)
+    pad: int
+    scale: float
+    kind: str = HADAMARD
+    seed: int = 0
+    phase_host: np.ndarray = None
+    sample_idx_host: np.ndarray = None
+
+    @property
+    def shape(self):
+        return (self.out_dim, self.in_dim)
+
+    @property
+    def field(self):
+        return REAL
+
+    @property
+    def mult(self):
+        # sketch.py:330 / :345: scale / sqrt(pad), one fp64 multiply per output
+        return self.scale / math.sqrt(self.pad)
+
+
+def build_fast_transform(k, l, kind, seed, device=None) -> FastTransformSketch:
+    """Draw a k x l subsampled fast transform (sketch.py:214-235)."""
+    if kind not in (FOURIER, HADAMARD):
+        raise ParameterError(f"unknown transform kind {kind!r}")
+    if kind == FOURIER:
+        raise NotImplementedError("the complex128 / FFT lane is out of scope of the B200 path")
+    if l < 1:
+        raise ParameterError(f"need l >= 1, got {l}")
+    pad = _next_pow2(l)
+    if not 1 <= k <= pad:
+        raise ParameterError(f"need 1 <= k <= {pad}, got k={k}")
+    seed = _check_seed(seed)
+    L = _lib.load()
+    phase = np.empty(l, dtype=np.float64)
+    idx = np.empty(k, dtype=np.int64)
+    padc = np.zeros(1, dtype=np.int64)
+    _lib.check(L.srlu_draw_fast_transform(seed, k, l, phase.ctypes.data, idx.ctypes.data,
+                                          padc.ctypes.data), "build_fast_transform")
+    assert int(padc[0]) == pad
+    dev = torch.device(device) if device is not None else _default_device()
+    phase_d = torch.from_numpy(phase).to(dev, non_blocking=False)
+    idx_d = torch.from_numpy(idx.astype(np.int32)).to(dev)
+    return FastTransformSketch(int(k), int(l), phase_d, idx_d, pad, math.sqrt(pad / k), kind,
+                               seed=seed, phase_host=phase, sample_idx_host=idx)
+
+
+@dataclass(frozen=True, eq=False)
+class CompositeSketch:
+    """sketch.py:238-266: sparse stage followed by the transform stage."""
+
+    sem: SparseEmbedding
+    fast: FastTransformSketch
+
+    def __post_init__(self):
+        if self.fast.in_dim != self.sem.out_dim:
+            raise ShapeError("stage mismatch between embedding and transform")
+
+    @property
+    def out_dim(self):
+        return self.fast.out_dim
+
+    @property
+    def in_dim(self):
+        return self.sem.in_dim
+
+    @property
+    def shape(self):
+        return (self.out_dim, self.in_dim)
+
+
+def build_composite(k, l, n, kind, seed, device=None) -> CompositeSketch:
+    """sketch.py:269-278 (transform stage seeded seed + 2**32)."""
+    return CompositeSketch(build_sem(l, n, seed, device),
+                           build_fast_transform(k, l, kind, seed + STAGE_SEED_OFFSET, device))
+
+
+# ---------------------------------------------------------------------------
+# application
+
+
+def _as_matrix(a):
+    return a if isinstance(a, Matrix) else Matrix(a)
+
+
+def sketch_right_into(a: Matrix, omega: CompositeSketch, y: torch.Tensor, nonfinite: torch.Tensor,
+                      stream=None):
+    """K1: y (m x k, fp64, row-major) = A · omega^*; nonfinite |= flag."""
+    L = _lib.lib()
+    sem, fast = omega.sem, omega.fast
+    m, n = a.shape
+    sh = _lib.stream_handle(stream)
+    if a.is_sparse:
+        indptr, indices, vals = a.raw
+        _lib.check(L.srlu_sketch_right_csr(
+            _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(vals), _lib.dtype_code(vals.dtype),
+            m, n, _lib.ptr(sem.row_of), _lib.ptr(sem.sign), sem.out_dim, _lib.ptr(fast.phase),
+            _lib.ptr(fast.sample_idx), fast.out_dim, fast.pad, fast.mult, _lib.ptr(y),
+            y.stride(0), _lib.ptr(nonfinite), sh), "sketch_right_csr")
+    else:
+        t = a.raw
+        srt, bptr = sem.plan()
+        _lib.check(L.srlu_sketch_right_dense(
+            _lib.ptr(t), _lib.dtype_code(t.dtype), m, n, t.stride(0), _lib.ptr(srt),
+            _lib.ptr(bptr), sem.out_dim, _lib.ptr(fast.phase), _lib.ptr(fast.sample_idx),
+            fast.out_dim, fast.pad, fast.mult, _lib.ptr(y), y.stride(0), _lib.ptr(nonfinite),
+            sh), "sketch_right_dense")
+
+
+def apply_sketch_right(a, omega: CompositeSketch) -> Matrix:
+    """``a @ omega^*`` (sketch.py:362-368), one fused kernel."""
+    a = _as_matrix(a)
+    if omega.in_dim != a.cols:
+        raise ShapeError(f"sketch expects {omega.in_dim} columns, got {a.cols}")
+    y = torch.empty(a.rows, omega.out_dim, dtype=torch.float64, device=a.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=a.device)
+    sketch_right_into(a, omega, y, flag)
+    if int(flag.item()):
+        raise ValueError("matrix entries must be finite")
+    return Matrix.from_device(y)
+
+
+def members(omega2: CompositeSketch, perm: torch.Tensor | None, row0: int, rows: int,
+            stream=None):
+    """Member table of the left sketch restricted to local rows [row0, row0+rows)."""
+    L = _lib.lib()
+    sem = omega2.sem
+    srt, bptr = sem.plan()
+    m = sem.in_dim
+    mrow = torch.empty(m, dtype=torch.int32, device=srt.device)
+    msign = torch.empty(m, dtype=torch.float64, device=srt.device)
+    _lib.check(L.srlu_sem_members(_lib.ptr(srt), m, _lib.ptr(perm), row0, rows, _lib.ptr(mrow),
+                                  _lib.ptr(msign), _lib.stream_handle(stream)), "sem_members")
+    return mrow, msign, bptr
+
+
+def sketch_left_into(a: Matrix, omega2: CompositeSketch, mrow, msign, bptr, outT: torch.Tensor,
+                     inv_perm=None, flags=None, stream=None):
+    """K3: outT (cols x k2) = (omega2 · P a)^T over a's (local) rows.
+    CSR: ``flags`` (int32 device scalar) gets bit 2 if a column is too long."""
+    L = _lib.lib()
+    fast = omega2.fast
+    sh = _lib.stream_handle(stream)
+    if a.is_sparse:
+        indptr, indices, vals = a.raw
+        nnz = vals.numel()
+        ws = _lib.workspace(L.srlu_sketch_left_csr_workspace(a.rows, a.cols, nnz,
+                                                             omega2.sem.out_dim, fast.pad),
+                            a.device)
+        _lib.check(L.srlu_sketch_left_csr(
+            _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(vals), _lib.dtype_code(vals.dtype),
+            a.rows, a.cols, nnz, _lib.ptr(inv_perm), _lib.ptr(omega2.sem.row_of),
+            _lib.ptr(omega2.sem.sign), omega2.sem.out_dim, _lib.ptr(fast.phase),
+            _lib.ptr(fast.sample_idx), fast.out_dim, fast.pad, fast.mult, _lib.ptr(outT),
+            outT.stride(0), _lib.ptr(ws), ws.numel(), _lib.ptr(flags), sh), "sketch_left_csr")
+        return
+    t = a.raw
+    ws = _lib.workspace(L.srlu_sketch_left_workspace(a.cols, omega2.sem.out_dim, fast.pad),
+                        a.device)
+    _lib.check(L.srlu_sketch_left_dense(
+        _lib.ptr(t), _lib.dtype_code(t.dtype), a.rows, a.cols, t.stride(0), _lib.ptr(mrow),
+        _lib.ptr(msign), _lib.ptr(bptr), omega2.sem.out_dim, _lib.ptr(fast.phase),
+        _lib.ptr(fast.sample_idx), fast.out_dim, fast.pad, fast.mult, _lib.ptr(outT),
+        outT.stride(0), _lib.ptr(ws), ws.numel(), sh), "sketch_left_dense")
+
+
+def apply_sketch_left(omega: CompositeSketch, a, perm=None) -> Matrix:
+    """``omega @ (P a)`` (sketch.py:371-378; P = identity when perm is None).
+    Returns the k x cols product (a transposed view of the kernel's
+    cols x k output)."""
+    a = _as_matrix(a)
+    if omega.in_dim != a.rows:
+        raise ShapeError(f"sketch expects {omega.in_dim} rows, got {a.rows}")
+    pd = None
+    if perm is not None:
+        pd = perm.device_indices(a.device) if hasattr(perm, "device_indices") else perm
+    outT = torch.empty(a.cols, omega.out_dim, dtype=torch.float64, device=a.device)
+    if a.is_sparse:
+        inv = None
+        if pd is not None:
+            inv = torch.empty(a.rows, dtype=torch.int32, device=a.device)
+            inv[pd] = torch.arange(a.rows, dtype=torch.int32, device=a.device)
+        else:
+            inv = torch.arange(a.rows, dtype=torch.int32, device=a.device)
+        flags = torch.zeros(1, dtype=torch.int32, device=a.device)
+        sketch_left_into(a, omega, None, None, None, outT, inv_perm=inv, flags=flags)
+        if int(flags.item()) & 2:
+            raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
+    else:
+        mrow, msign, bptr = members(omega, pd, 0, a.rows)
+        sketch_left_into(a, omega, mrow, msign, bptr, outT)
+    return Matrix.from_device(outT.t())

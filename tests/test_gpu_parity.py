@@ -1,0 +1,300 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Bit-exact: draws, the bucket plan, Y (stage-1 sketch), P, L1, both stage-2
+reductions, Q.  Tolerance (north star): L and U within 1e-10 relative
+(Frobenius) of the reference, ||LU - PAQ||_F within 1%.  Golden vectors
+were produced by the reference itself (tests/golden/make_golden.py)."""
+
+import hashlib
+import logging
+
+import numpy as np
+import pytest
+
+from tests.conftest import cuda_ok
+from tests.golden import cases
+
+pytestmark = pytest.mark.gpu
+
+LU_RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not cuda_ok():
+        pytest.skip("needs a CUDA device")
+    import paper_1601_04280_b200 as pkg
+    return pkg
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _np(t):
+    import torch
+    if isinstance(t, torch.Tensor):
+        return t.detach().cpu().numpy()
+    if hasattr(t, "numpy"):
+        return t.numpy()
+    return np.asarray(t)
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# --------------------------------------------------------------------------
+# K0 draws
+
+
+@pytest.mark.parametrize("name", list(cases.DRAW_SHAPES))
+def test_device_draws_match_reference(P, golden, name):
+    g = golden("draws.npz")
+    k, l, n, seed = cases.DRAW_SHAPES[name]
+    om = P.build_composite(k, l, n, "hadamard", seed)
+    row_of = _np(om.sem.row_of).astype(np.int64)
+    sign = _np(om.sem.sign)
+    assert _sha(row_of) == g[name + "_row_of_sha"].item().decode()
+    assert _sha(sign) == g[name + "_sign_sha"].item().decode()
+    np.testing.assert_array_equal(_np(om.fast.phase), g[name + "_phase"])
+    np.testing.assert_array_equal(_np(om.fast.sample_idx), g[name + "_idx"])
+    assert om.fast.pad == int(g[name + "_pad"]) and om.fast.scale == float(g[name + "_scale"])
+
+
+def test_draws_rejection_heavy_range(P):
+    # l = 2^20 buckets: ~500 Lemire rejections in 2^21 draws; the device
+    # position remapping must match numpy's sequential stream exactly
+    l, n, seed = 2 ** 20, 2 ** 21, 77
+    om = P.build_sem(l, n, seed)
+    g = np.random.Generator(np.random.Philox(seed))
+    np.testing.assert_array_equal(_np(om.row_of), g.integers(0, l, size=n))
+    np.testing.assert_array_equal(_np(om.sign), (g.integers(0, 2, size=n) * 2 - 1).astype(float))
+
+
+def test_sem_plan_is_stable_bucket_sort(P):
+    sem = P.build_sem(97, 20000, 5)
+    srt, bptr = sem.plan()
+    srt, bptr = _np(srt), _np(bptr)
+    row_of, sign = _np(sem.row_of), _np(sem.sign)
+    src = srt & 0x7FFFFFFF
+    neg = srt < 0
+    assert np.array_equal(np.diff(bptr), np.bincount(row_of, minlength=97))
+    for t in range(97):
+        seg = src[bptr[t]:bptr[t + 1]]
+        assert np.all(np.diff(seg) > 0)
+        assert np.all(row_of[seg] == t)
+    assert np.array_equal(neg, sign[src] < 0)
+
+
+# --------------------------------------------------------------------------
+# the plugin seam (_kernels) against the reference's own kernel outputs
+
+
+def test_kernel_seam_matches_reference(P, golden):
+    import torch
+    from paper_1601_04280_b200 import _kernels as K
+    g = golden("kernels.npz")
+    for name, case in cases.kernel_cases().items():
+        kind = case["kind"]
+        if kind == "fwht":
+            x = torch.tensor(case["x"], device="cuda")
+            K.fwht_rows(x)
+            got = x
+        elif kind == "gather_dense":
+            out = torch.zeros(case["out_shape"], dtype=torch.float64, device="cuda")
+            K.sem_gather_dense(torch.tensor(case["a"], device="cuda"), case["row_of"],
+                               case["sign"], out)
+            got = out
+        elif kind == "scatter_dense":
+            out = torch.zeros(case["out_shape"], dtype=torch.float64, device="cuda")
+            K.sem_scatter_dense(torch.tensor(case["a"], device="cuda"), case["row_of"],
+                                case["sign"], out)
+            got = out
+        else:
+            sp = case["csc"]
+            out = torch.zeros(case["out_shape"], dtype=torch.float64, device="cuda")
+            fn = K.sem_gather_csc if kind == "gather_csc" else K.sem_scatter_csc
+            fn(torch.tensor(sp.data), torch.tensor(sp.indices), torch.tensor(sp.indptr),
+               case["row_of"], case["sign"], out)
+            got = out
+        np.testing.assert_array_equal(_np(got), g[name], err_msg=name)
+
+
+# --------------------------------------------------------------------------
+# K2 / K5 pivoted LUs against the reference's factor.py
+
+
+def test_factor_matches_reference(P, golden):
+    g = golden("factor.npz")
+    for name, b in cases.factor_cases().items():
+        if b.shape[0] >= b.shape[1]:
+            r = P.lu_row_pivot(b)
+            np.testing.assert_array_equal(r.P.indices, g[name + "_row_P"], err_msg=name)
+            np.testing.assert_array_equal(r.L.numpy(), g[name + "_row_L"], err_msg=name)
+            np.testing.assert_array_equal(r.U.numpy(), g[name + "_row_U"], err_msg=name)
+        bt = b.T if b.shape[0] >= b.shape[1] else b
+        c = P.lu_col_pivot(bt)
+        np.testing.assert_array_equal(c.Q.indices, g[name + "_col_Q"], err_msg=name)
+        np.testing.assert_array_equal(c.L.numpy(), g[name + "_col_L"], err_msg=name)
+        np.testing.assert_array_equal(c.U.numpy(), g[name + "_col_U"], err_msg=name)
+
+
+@pytest.mark.parametrize("m,k,seed,ints", [(20000, 200, 1, False), (6000, 150, 2, True),
+                                           (3001, 97, 3, False), (40000, 64, 4, False)])
+def test_lu_row_pivot_panels_bit_exact(P, m, k, seed, ints):
+    """Sizes that force several panels + deferred trailing updates."""
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(seed))
+    b = g.integers(-3, 4, size=(m, k)).astype(np.float64) if ints else g.standard_normal((m, k))
+    perm, lo, up = O.lu_row_pivot(b)
+    r = P.lu_row_pivot(b)
+    np.testing.assert_array_equal(r.P.indices, perm)
+    np.testing.assert_array_equal(r.L.numpy(), lo)
+    np.testing.assert_array_equal(r.U.numpy(), up)
+
+
+@pytest.mark.parametrize("k,n,seed", [(150, 30000, 5), (97, 5003, 6), (40, 100000, 7)])
+def test_lu_col_pivot_panels_bit_exact(P, k, n, seed):
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(seed))
+    c = g.standard_normal((k, n))
+    q, lo, up = O.lu_col_pivot(c)
+    r = P.lu_col_pivot(c)
+    np.testing.assert_array_equal(r.Q.indices, q)
+    np.testing.assert_array_equal(r.L.numpy(), lo)
+    np.testing.assert_array_equal(r.U.numpy(), up)
+
+
+def test_lu_low_rank_threshold_path(P):
+    """Exactly low rank: later pivots fall under PIVOT_RTOL*||B||_F."""
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(11))
+    b = g.standard_normal((5000, 6)) @ g.standard_normal((6, 40))
+    perm, lo, up = O.lu_row_pivot(b)
+    r = P.lu_row_pivot(b)
+    np.testing.assert_array_equal(r.P.indices, perm)
+    np.testing.assert_array_equal(r.L.numpy(), lo)
+    q, lo2, up2 = O.lu_col_pivot(b[:40].T.copy())
+    c = P.lu_col_pivot(b[:40].T.copy())
+    np.testing.assert_array_equal(c.Q.indices, q)
+    np.testing.assert_array_equal(c.L.numpy(), lo2)
+
+
+# --------------------------------------------------------------------------
+# the whole path against the reference's outputs (golden)
+
+PIPES = ["small_dense", "ragged", "sparse", "zero", "lowrank_resample", "tall_f32",
+         "sparse_wide", "cfg1"]
+
+
+def _input(P, a, as_f32=False):
+    import torch
+    if hasattr(a, "tocsr"):
+        return P.Matrix.sparse(a)
+    t = torch.tensor(np.ascontiguousarray(a), device="cuda")
+    if as_f32:
+        t = t.float()
+    return P.Matrix.from_device(t)
+
+
+@pytest.mark.parametrize("name", PIPES)
+def test_pipeline_matches_reference(P, golden, name):
+    g = golden(f"pipe_{name}.npz")
+    a, prm = cases.pipeline_cases()[name]
+    # tall_f32 holds float32-representable values: feed it as float32 storage
+    mat = _input(P, a, as_f32=(name == "tall_f32"))
+    res = P.sparse_randomized_lu(mat, P.RandLuParams(**prm), keep=True)
+    ex = res.extras
+    assert res.attempt == int(g["attempt"])
+    np.testing.assert_array_equal(_np(ex["Y"]), g["Y"])
+    np.testing.assert_array_equal(res.P.indices, g["P"])
+    if "L1" in g:
+        np.testing.assert_array_equal(_np(ex["L1"]), g["L1"])
+    np.testing.assert_array_equal(_np(ex["red_l"]), g["red_l"])
+    np.testing.assert_array_equal(_np(ex["red_a"]), g["red_a"])
+    np.testing.assert_array_equal(res.Q.indices, g["Q"])
+    assert _rel(_np(ex["core"]), g["core"]) <= 1e-12
+    assert _rel(res.L.numpy(), g["L"]) <= LU_RTOL
+    assert _rel(res.U.numpy(), g["U"]) <= LU_RTOL
+    err = P.approximation_error(mat, res)
+    want = float(g["err"])
+    if want == 0.0:
+        assert err == 0.0
+    else:
+        assert abs(err - want) <= 0.01 * want
+    assert set(res.elapsed) == {"sketch1", "lu1", "sketch2", "pinv", "lu2", "total"}
+
+
+def test_resample_warnings(P, caplog):
+    a, prm = cases.pipeline_cases()["lowrank_resample"]
+    with caplog.at_level(logging.WARNING, logger="paper_1601_04280_b200.randlu"):
+        res = P.sparse_randomized_lu(a, P.RandLuParams(**prm))
+    assert res.attempt == 2
+    assert sum("resampling" in r.message for r in caplog.records) == 2
+
+
+def test_determinism_bit_identical(P):
+    a, prm = cases.pipeline_cases()["small_dense"]
+    r1 = P.sparse_randomized_lu(a, P.RandLuParams(**prm))
+    r2 = P.sparse_randomized_lu(a, P.RandLuParams(**prm))
+    assert np.array_equal(r1.P.indices, r2.P.indices)
+    assert np.array_equal(r1.Q.indices, r2.Q.indices)
+    np.testing.assert_array_equal(r1.L.numpy(), r2.L.numpy())
+    np.testing.assert_array_equal(r1.U.numpy(), r2.U.numpy())
+
+
+def test_zero_matrix_zero_error(P):
+    a = np.zeros((60, 50))
+    res = P.sparse_randomized_lu(a, P.RandLuParams(r=2, k1=3, l1=20, k2=4, l2=48, seed=1))
+    assert P.approximation_error(a, res) == 0.0
+    assert np.all(res.U.numpy() == 0.0)
+
+
+def test_non_finite_rejected(P):
+    import torch
+    a = torch.randn(200, 150, device="cuda", dtype=torch.float64)
+    a[17, 33] = float("nan")
+    with pytest.raises(ValueError, match="finite"):
+        P.sparse_randomized_lu(P.Matrix.from_device(a), P.default_params(5, 200, 150))
+    a[17, 33] = float("inf")
+    with pytest.raises(ValueError, match="finite"):
+        P.sparse_randomized_lu(P.Matrix.from_device(a), P.default_params(5, 200, 150))
+
+
+def test_params_checked_against_matrix(P):
+    with pytest.raises(P.ParameterError):
+        P.sparse_randomized_lu(np.zeros((30, 30)), P.RandLuParams(r=2, k1=3, l1=40, k2=4, l2=20))
+
+
+def test_exact_rank_recovery(P):
+    from tests.golden.cases import gen_rank_noise
+    for seed in range(3):
+        a = gen_rank_noise(300, 300, 10, 0.0, seed)
+        res = P.sparse_randomized_lu(a, P.default_params(10, 300, 300, seed=100 + seed))
+        assert P.approximation_error(a, res) <= 1e-8 * np.linalg.norm(a)
+
+
+# --------------------------------------------------------------------------
+# BASELINE config 2 at full size against the CPU oracle (same fp32 input)
+
+
+@pytest.mark.slow
+def test_config2_full_size_vs_oracle(P):
+    import torch
+    from threadpoolctl import threadpool_limits
+    from oracle import randlu as O
+    from bench import gen_config
+    a, prm = gen_config(2)
+    res = P.sparse_randomized_lu(P.Matrix.from_device(a), P.RandLuParams(**prm), keep=True)
+    host = a.double().cpu().numpy()
+    with threadpool_limits(8):
+        ref = O.sparse_randomized_lu(host, prm, keep=True)
+    np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
+    np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
+    np.testing.assert_array_equal(res.Q.indices, ref["Q"])
+    assert _rel(res.L.numpy(), ref["L"]) <= LU_RTOL
+    assert _rel(res.U.numpy(), ref["U"]) <= LU_RTOL
