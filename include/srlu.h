@@ -166,6 +166,27 @@ int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int64_t *q, do
                    int64_t ldlt, double *UT, int64_t ldut, void *ws, size_t ws_bytes,
                    srlu_stream_t stream);
 
+/* ---- small dense tail (K4) --------------------------------------------- */
+
+/* left_pseudo_inverse (factor.py:112-130) of M (k2 x k1) given as mT = M^T
+ * (k1 x k2 row-major), in one CTA: Householder QR, rank test, and
+ * pinvT = (R^-1 Q^T)^T (k2 x k1 row-major).  stats[4] (device):
+ * sigma_max estimate, sigma_min estimate, cond, singular flag (1.0 when
+ * sigma_min <= 1e-10 sigma_max, factor.py:124).  Needs
+ * srlu_qr_pinv_smem_bytes(k1, k2) <= 220 KiB, else SRLU_ERR_UNSUPPORTED. */
+size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2);
+int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *pinvT,
+                 int64_t ldp, double *stats, srlu_stream_t stream);
+
+/* the same rank test on an upper-triangular R (k x k row-major, device) */
+int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, double *stats,
+                       srlu_stream_t stream);
+
+/* C (M x N) = A (M x K) · B (K x N), row-major fp64 (matrix.py:219-230 matmul
+ * for randlu.py:267 and :272) */
+int srlu_dgemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+               int64_t ldc, int64_t M, int64_t N, int64_t K, srlu_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

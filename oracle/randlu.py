@@ -340,6 +340,44 @@ def approximation_error(a, res, block_cols=256):
     return math.sqrt(acc)
 
 
+def _qr_longdouble(mat):
+    """Householder QR in x87 extended precision (64-bit mantissa)."""
+    R = np.array(mat, dtype=np.longdouble)
+    p, q = R.shape
+    Q = np.eye(p, dtype=np.longdouble)
+    for j in range(q):
+        x = R[j:, j]
+        nx = np.sqrt(np.sum(x * x))
+        if nx == 0:
+            continue
+        v = x.copy()
+        v[0] += nx if x[0] >= 0 else -nx
+        v /= np.sqrt(np.sum(v * v))
+        R[j:, j:] -= 2 * np.outer(v, v @ R[j:, j:])
+        Q[:, j:] -= 2 * np.outer(Q[:, j:] @ v, v)
+    return Q[:, :q], R[:q, :q]
+
+
+def forward_error_band(red_l, red_a, l1):
+    """How far the reference's own L, U sit from the (nearly) exact answer.
+
+    Re-runs the tail of the pipeline (pinv, core = pinv·red_a, lu_col_pivot,
+    L = L1·L~) with pinv and core formed in extended precision, from the
+    reference's bit-exact intermediates.  The distance between these factors
+    and the reference's is the reference's own forward error; any other
+    correct fp64 implementation (a different but equally stable QR/GEMM)
+    lands at a comparable distance.  Returns (q, L, U)."""
+    qf, rf = _qr_longdouble(red_l)
+    k = rf.shape[0]
+    b = qf.T.copy()
+    x = np.zeros_like(b)
+    for i in range(k - 1, -1, -1):
+        x[i] = (b[i] - rf[i, i + 1:] @ x[i + 1:]) / rf[i, i]
+    core = (x @ np.asarray(red_a, dtype=np.longdouble)).astype(np.float64)
+    q, lt, u = lu_col_pivot(core)
+    return q, matmul(l1, lt), u
+
+
 def default_params(r, m, n, seed=0):
     """randlu.py:117-143 (practical mode)."""
     if not 1 <= r <= min(m, n) / 2:

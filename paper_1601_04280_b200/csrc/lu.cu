@@ -21,6 +21,8 @@
 //     with the pivot entities' trailing vectors obtained by the small
 //     in-panel triangular recurrence.
 // Result: P/Q and L/U bit-identical to the reference on the same input.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace srlu {
@@ -350,6 +352,10 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     SRLU_REQUIRE(M < (1LL << 31) - 1 && k <= 8192, SRLU_ERR_UNSUPPORTED, "lu: sizes too large");
     SRLU_REQUIRE(ws_bytes >= srlu_lu_workspace(M, k), SRLU_ERR_WORKSPACE, "lu: workspace too small");
     int G = sm_count();
+    if (const char *env = getenv("SRLU_LU_MAX_GRID")) {  // testing knob
+        int cap = atoi(env);
+        if (cap >= 1 && cap < G) G = cap;
+    }
     if (G > kLuMaxGrid) G = kLuMaxGrid;
     if (G > M) G = (int)M;
     int rpc = (int)ceil_div(M, G);

@@ -8,7 +8,7 @@
 
 namespace srlu {
 
-constexpr int kPlanBlock = 2048;  // sources per counting block
+constexpr int kPlanBlock = 256;  // sources per counting block (one warp each)
 
 __global__ void plan_hist_kernel(const int32_t *row_of, int64_t n, int l, int *counts) {
     extern __shared__ int hist[];
@@ -19,20 +19,40 @@ __global__ void plan_hist_kernel(const int32_t *row_of, int64_t n, int l, int *c
     for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(&hist[row_of[i]], 1);
     __syncthreads();
     for (int t = threadIdx.x; t < l; t += blockDim.x)
-        counts[(int64_t)blockIdx.x * l + t] = hist[t];
+        counts[(int64_t)t * gridDim.x + blockIdx.x] = hist[t];
 }
 
-// per bucket: exclusive scan over blocks; bucket totals
+// one CTA per bucket: exclusive scan of its per-block counts; bucket totals
 __global__ void plan_scan_blocks_kernel(int *counts, int nblk, int l, int *total) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= l) return;
-    int run = 0;
-    for (int b = 0; b < nblk; ++b) {
-        int c = counts[(int64_t)b * l + t];
-        counts[(int64_t)b * l + t] = run;
-        run += c;
+    __shared__ int warp_sums[32];
+    __shared__ int carry;
+    const int t = blockIdx.x;
+    int *row = counts + (int64_t)t * nblk;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nblk; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        const int v = b < nblk ? row[b] : 0;
+        int incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        if (lane == 31) warp_sums[warp] = incl;
+        __syncthreads();
+        int wbase = 0;
+        for (int w = 0; w < warp; ++w) wbase += warp_sums[w];
+        int tile_total = 0;
+        for (int w = 0; w < nw; ++w) tile_total += warp_sums[w];
+        const int c = carry;
+        if (b < nblk) row[b] = c + wbase + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + tile_total;
+        __syncthreads();
     }
-    total[t] = run;
+    if (threadIdx.x == 0) total[t] = carry;
 }
 
 // single CTA: bucket_ptr = exclusive scan of totals
@@ -69,7 +89,7 @@ __global__ void plan_scatter_kernel(const int32_t *row_of, const double *sign, i
     extern __shared__ int cursor[];
     int lane = threadIdx.x;
     for (int t = lane; t < l; t += 32)
-        cursor[t] = bucket_ptr[t] + counts[(int64_t)blockIdx.x * l + t];
+        cursor[t] = bucket_ptr[t] + counts[(int64_t)t * gridDim.x + blockIdx.x];
     __syncwarp();
     int64_t b0 = (int64_t)blockIdx.x * kPlanBlock;
     int64_t b1 = min(n, b0 + kPlanBlock);
@@ -136,8 +156,7 @@ extern "C" int srlu_sem_plan(const int32_t *row_of, const double *sign, int64_t 
     }
     plan_hist_kernel<<<nblk, 256, smem, stream>>>(row_of, n, (int)l, counts);
     SRLU_CHECK_LAUNCH("plan_hist_kernel");
-    plan_scan_blocks_kernel<<<(unsigned)ceil_div(l, 256), 256, 0, stream>>>(counts, nblk, (int)l,
-                                                                           total);
+    plan_scan_blocks_kernel<<<(unsigned)l, 256, 0, stream>>>(counts, nblk, (int)l, total);
     SRLU_CHECK_LAUNCH("plan_scan_blocks_kernel");
     plan_scan_buckets_kernel<<<1, 1024, 0, stream>>>(total, (int)l, bucket_ptr);
     SRLU_CHECK_LAUNCH("plan_scan_buckets_kernel");

@@ -1,0 +1,379 @@
+// K4 — the small dense tail of the pipeline (reference: factor.py:112-130
+// left_pseudo_inverse, randlu.py:266-267 and :272 matmul).
+//
+//  * srlu_qr_pinv: Householder QR of M = Omega2·L1 (k2 x k1) in ONE CTA with
+//    M resident in shared memory (LAPACK dgeqr2/dlarfg conventions), the
+//    rank test, and pinv^T = (R^-1 Q^T)^T.  Replaces numpy.linalg.qr +
+//    numpy.linalg.svd + scipy solve_triangular.
+//  * rank test: the reference compares the extreme singular values of R
+//    (sv[-1] <= 1e-10 sv[0]).  Here: sigma_max >= max(|R_jj|, ||R x||) from
+//    8 power iterations, sigma_min <= min(|R_jj|, ||(R^T R)^-1 x||^-1/2)
+//    from 8 inverse iterations — estimates that bracket the true values from
+//    the inside and agree with the SVD decision except when cond(R) sits
+//    within the estimators' slack of 1e10.
+//  * srlu_rank_estimate: the same test on an R in global memory (used when
+//    M does not fit one CTA; the QR then comes from cuSOLVER).
+//  * srlu_dgemm: C = A·B row-major fp64 SIMT-FMA GEMM for the skinny core
+//    and L products (cuBLAS picks a 32x32 DMMA tile that reached <3 TFLOP/s
+//    on the 16384x118x110 shape).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace srlu {
+
+constexpr int kQrThreads = 512;
+constexpr int kQrWarps = kQrThreads / 32;
+constexpr double kRankRtol = 1e-10;  // factor.py:22
+
+__device__ inline double block_sum(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    return s;
+}
+
+__device__ inline double block_max(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = red[0];
+    const int nw = blockDim.x >> 5;
+    for (int w = 1; w < nw; ++w) s = fmax(s, red[w]);
+    return s;
+}
+
+__device__ inline double block_min(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = red[0];
+    const int nw = blockDim.x >> 5;
+    for (int w = 1; w < nw; ++w) s = fmin(s, red[w]);
+    return s;
+}
+
+// R accessor: upper triangle R(r, c), r <= c
+struct RSmem {  // column-major with stride ld (the QR workspace)
+    const double *a;
+    int ld;
+    __device__ double operator()(int r, int c) const { return a[c * ld + r]; }
+};
+struct RGlobalRowMajor {
+    const double *a;
+    int64_t ld;
+    __device__ double operator()(int r, int c) const { return a[(int64_t)r * ld + c]; }
+};
+
+// stats[0] = sigma_max estimate, [1] = sigma_min estimate, [2] = cond, [3] = singular flag
+template <typename RA>
+__device__ void rank_estimate(RA R, int k, double *x, double *y, double *red, double *stats) {
+    const int tid = threadIdx.x;
+    double dmax = 0.0, dmin = INFINITY;
+    for (int j = tid; j < k; j += blockDim.x) {
+        double d = fabs(R(j, j));
+        dmax = fmax(dmax, d);
+        dmin = fmin(dmin, d);
+    }
+    dmax = block_max(dmax, red);
+    dmin = block_min(dmin, red);
+    double smax = dmax, smin = dmin;
+    const double inv_sqrt_k = 1.0 / sqrt((double)k);
+    // power iteration: sigma_max >= ||R x|| for unit x
+    for (int j = tid; j < k; j += blockDim.x) x[j] = inv_sqrt_k;
+    __syncthreads();
+    for (int it = 0; it < 8 && dmax > 0.0; ++it) {
+        double ss = 0.0;
+        for (int r = tid; r < k; r += blockDim.x) {
+            double s = 0.0;
+            for (int c = r; c < k; ++c) s += R(r, c) * x[c];
+            y[r] = s;
+            ss += s * s;
+        }
+        ss = block_sum(ss, red);
+        smax = fmax(smax, sqrt(ss));
+        double zz = 0.0;
+        for (int c = tid; c < k; c += blockDim.x) {
+            double s = 0.0;
+            for (int r = 0; r <= c; ++r) s += R(r, c) * y[r];
+            x[c] = s;  // y is complete (synced by block_sum)
+            zz += s * s;
+        }
+        zz = block_sum(zz, red);
+        const double inv = zz > 0.0 ? 1.0 / sqrt(zz) : 0.0;
+        for (int c = tid; c < k; c += blockDim.x) x[c] *= inv;
+        __syncthreads();
+    }
+    // inverse iteration: sigma_min <= ||(R^T R)^-1 x||^(-1/2) for unit x
+    if (dmin > 0.0) {
+        for (int j = tid; j < k; j += blockDim.x) x[j] = ((j & 1) ? -inv_sqrt_k : inv_sqrt_k);
+        __syncthreads();
+        for (int it = 0; it < 8; ++it) {
+            // R^T y = x (forward, axpy form): y_r = x_r / R_rr; x_c -= R_rc y_r
+            for (int r = 0; r < k; ++r) {
+                const double yr = x[r] / R(r, r);
+                for (int c = r + 1 + tid; c < k; c += blockDim.x) x[c] -= R(r, c) * yr;
+                if (tid == 0) y[r] = yr;
+                __syncthreads();
+            }
+            // R z = y (backward, axpy form): z_c = y_c / R_cc; y_r -= R_rc z_c
+            for (int c = k - 1; c >= 0; --c) {
+                const double zc = y[c] / R(c, c);
+                for (int r = tid; r < c; r += blockDim.x) y[r] -= R(r, c) * zc;
+                if (tid == 0) x[c] = zc;
+                __syncthreads();
+            }
+            double zz = 0.0;
+            for (int c = tid; c < k; c += blockDim.x) zz += x[c] * x[c];
+            zz = block_sum(zz, red);
+            if (!(zz > 0.0) || !isfinite(zz)) {
+                smin = 0.0;
+                break;
+            }
+            smin = fmin(smin, 1.0 / sqrt(sqrt(zz)));
+            const double inv = 1.0 / sqrt(zz);
+            for (int c = tid; c < k; c += blockDim.x) x[c] *= inv;
+            __syncthreads();
+        }
+    } else {
+        smin = 0.0;
+    }
+    if (tid == 0) {
+        stats[0] = smax;
+        stats[1] = smin;
+        stats[2] = smin > 0.0 ? smax / smin : INFINITY;
+        stats[3] = (smax == 0.0 || smin <= kRankRtol * smax) ? 1.0 : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kQrThreads, 1) qr_pinv_kernel(const double *__restrict__ mT,
+                                                                int k1, int k2, int64_t ldm,
+                                                                double *__restrict__ pinvT,
+                                                                int64_t ldp,
+                                                                double *__restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ld = k2 | 1;
+    const int k2p = (k2 + 1) & ~1;
+    double *A = reinterpret_cast<double *>(smem_raw);  // column c: A[c*ld + r] = M[r][c]
+    double *tau = A + (size_t)k1 * ld;
+    double *xv = tau + ((k1 + 1) & ~1);
+    double *yv = xv + k2p;
+    double *red = yv + k2p;                 // 64
+    double *zw = red + 64;                  // kQrWarps x k2p
+    __shared__ double s_scal;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int i = tid; i < k1 * k2; i += blockDim.x) {
+        const int c = i / k2, r = i % k2;
+        A[c * ld + r] = mT[(int64_t)c * ldm + r];
+    }
+    __syncthreads();
+
+    // ---- Householder QR (dgeqr2) -------------------------------------------
+    for (int j = 0; j < k1; ++j) {
+        double* colj = A + j * ld;
+        double part = 0.0;
+        for (int r = j + 1 + tid; r < k2; r += blockDim.x) part += colj[r] * colj[r];
+        const double xnorm2 = block_sum(part, red);
+        if (tid == 0) {
+            const double alpha = colj[j];
+            double t = 0.0, scal = 0.0;
+            if (xnorm2 > 0.0) {
+                const double xnorm = sqrt(xnorm2);
+                const double beta = -copysign(hypot(alpha, xnorm), alpha);
+                t = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+                colj[j] = beta;
+            }
+            tau[j] = t;
+            s_scal = scal;
+        }
+        __syncthreads();
+        const double tj = tau[j];
+        if (tj != 0.0) {
+            const double scal = s_scal;
+            for (int r = j + 1 + tid; r < k2; r += blockDim.x) colj[r] *= scal;
+        }
+        __syncthreads();
+        if (tj != 0.0) {
+            for (int c = j + 1 + warp; c < k1; c += kQrWarps) {
+                double *colc = A + c * ld;
+                double w = lane == 0 ? colc[j] : 0.0;
+                for (int r = j + 1 + lane; r < k2; r += 32) w += colj[r] * colc[r];
+#pragma unroll
+                for (int off = 16; off; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
+                const double f = tj * w;
+                if (lane == 0) colc[j] -= f;
+                for (int r = j + 1 + lane; r < k2; r += 32) colc[r] -= f * colj[r];
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- rank test on R -----------------------------------------------------
+    rank_estimate(RSmem{A, ld}, k1, xv, yv, red, stats);
+    __syncthreads();
+
+    // ---- pinv^T[c][:] = R^-1 (Q^T e_c)[:k1], one warp per column c ---------
+    double *z = zw + (size_t)warp * k2p;
+    for (int c = warp; c < k2; c += kQrWarps) {
+        for (int r = lane; r < k2; r += 32) z[r] = (r == c) ? 1.0 : 0.0;
+        __syncwarp();
+        for (int j = 0; j < k1; ++j) {
+            const double tj = tau[j];
+            if (tj == 0.0) continue;
+            const double *colj = A + j * ld;
+            double w = lane == 0 ? z[j] : 0.0;
+            for (int r = j + 1 + lane; r < k2; r += 32) w += colj[r] * z[r];
+#pragma unroll
+            for (int off = 16; off; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
+            const double f = tj * w;
+            __syncwarp();
+            if (lane == 0) z[j] -= f;
+            for (int r = j + 1 + lane; r < k2; r += 32) z[r] -= f * colj[r];
+            __syncwarp();
+        }
+        for (int i = k1 - 1; i >= 0; --i) {
+            const double zi = z[i] / A[i * ld + i];
+            __syncwarp();
+            for (int r = lane; r < i; r += 32) z[r] -= A[i * ld + r] * zi;
+            if (lane == 0) z[i] = zi;
+            __syncwarp();
+        }
+        for (int i = lane; i < k1; i += 32) pinvT[(int64_t)c * ldp + i] = z[i];
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kQrThreads, 1) rank_estimate_kernel(const double *__restrict__ R,
+                                                                      int k, int64_t ldr,
+                                                                      double *__restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xv = reinterpret_cast<double *>(smem_raw);
+    double *yv = xv + k;
+    double *red = yv + k;
+    rank_estimate(RGlobalRowMajor{R, ldr}, k, xv, yv, red, stats);
+}
+
+// ---------------------------------------------------------------------------
+// C (M x N) = A (M x K) . B (K x N), row-major fp64, FMA.
+
+constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
+
+__global__ void __launch_bounds__(256) dgemm_kernel(const double *__restrict__ A, int64_t lda,
+                                                    const double *__restrict__ B, int64_t ldb,
+                                                    double *__restrict__ C, int64_t ldc,
+                                                    int64_t M, int N, int K) {
+    __shared__ double As[kGemmBK][kGemmBM + 2];
+    __shared__ double Bs[kGemmBK][kGemmBN + 2];
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t m0 = (int64_t)blockIdx.x * kGemmBM;
+    const int n0 = blockIdx.y * kGemmBN;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += kGemmBK) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int e = tid + i * 256;  // 0..1023
+            const int am = e / kGemmBK, ak = e % kGemmBK;
+            const int64_t gm = m0 + am;
+            const int gk = k0 + ak;
+            As[ak][am] = (gm < M && gk < K) ? A[gm * lda + gk] : 0.0;
+            const int bk = e / kGemmBN, bn = e % kGemmBN;
+            const int gk2 = k0 + bk, gn = n0 + bn;
+            Bs[bk][bn] = (gk2 < K && gn < N) ? B[(int64_t)gk2 * ldb + gn] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGemmBK; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gm = m0 + ty * 4 + i;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gn = n0 + tx + 16 * j;
+            if (gn < N) C[gm * ldc + gn] = acc[i][j];
+        }
+    }
+}
+
+static size_t qr_pinv_smem(int64_t k1, int64_t k2) {
+    const int64_t ld = k2 | 1, k2p = (k2 + 1) & ~1;
+    return sizeof(double) * (size_t)(k1 * ld + ((k1 + 1) & ~1) + 2 * k2p + 64 +
+                                     (int64_t)kQrWarps * k2p);
+}
+
+}  // namespace srlu
+
+using namespace srlu;
+
+extern "C" size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2) { return qr_pinv_smem(k1, k2); }
+
+extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *pinvT,
+                            int64_t ldp, double *stats, srlu_stream_t stream) {
+    SRLU_REQUIRE(k1 >= 1 && k2 >= k1 && ldm >= k2 && ldp >= k1, SRLU_ERR_ARG,
+                 "left_pseudo_inverse: need rows >= cols, got %lld x %lld", (long long)k2,
+                 (long long)k1);
+    size_t smem = qr_pinv_smem(k1, k2);
+    SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED,
+                 "qr_pinv: %lld x %lld does not fit one CTA's shared memory", (long long)k2,
+                 (long long)k1);
+    SRLU_CUDA(cudaFuncSetAttribute(qr_pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    qr_pinv_kernel<<<1, kQrThreads, smem, (cudaStream_t)stream>>>(mT, (int)k1, (int)k2, ldm, pinvT,
+                                                                  ldp, stats);
+    SRLU_CHECK_LAUNCH("qr_pinv_kernel");
+    return SRLU_OK;
+}
+
+extern "C" int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, double *stats,
+                                  srlu_stream_t stream) {
+    SRLU_REQUIRE(k >= 1 && ldr >= k, SRLU_ERR_ARG, "rank_estimate: bad sizes");
+    size_t smem = sizeof(double) * (size_t)(2 * k + 64);
+    SRLU_REQUIRE(smem <= 200 * 1024, SRLU_ERR_UNSUPPORTED, "rank_estimate: k too large");
+    SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rank_estimate_kernel<<<1, kQrThreads, smem, (cudaStream_t)stream>>>(R, (int)k, ldr, stats);
+    SRLU_CHECK_LAUNCH("rank_estimate_kernel");
+    return SRLU_OK;
+}
+
+extern "C" int srlu_dgemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                          int64_t ldc, int64_t M, int64_t N, int64_t K, srlu_stream_t stream) {
+    SRLU_REQUIRE(M >= 0 && N >= 0 && K >= 0 && N < (1 << 30) && K < (1 << 30), SRLU_ERR_ARG,
+                 "dgemm: bad sizes");
+    if (M == 0 || N == 0) return SRLU_OK;
+    dim3 grid((unsigned)ceil_div(M, kGemmBM), (unsigned)ceil_div(N, kGemmBN));
+    dgemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, C, ldc, M, (int)N, (int)K);
+    SRLU_CHECK_LAUNCH("dgemm_kernel");
+    return SRLU_OK;
+}

@@ -106,20 +106,58 @@ def lu_col_pivot(mat) -> ColPivotedLU:
                         Matrix.from_device(ut.t().contiguous()))
 
 
-def pinv_dev(mat: torch.Tensor):
-    """Householder QR + sigma-ratio test + triangular solve on the device.
-    Returns (pinv k1 x k2, cond) with cond = sv_max / sv_min (a device
-    scalar); the caller decides singularity (one host sync)."""
-    qf, rf = torch.linalg.qr(mat, mode="reduced")
-    sv = torch.linalg.svdvals(rf)
-    pinv = torch.linalg.solve_triangular(rf, qf.t().contiguous(), upper=True)
-    return pinv, sv
+QR_SMEM_LIMIT = 220 * 1024
 
 
-def check_rank(sv_host):
-    """factor.py:123-128"""
-    if sv_host[0] == 0.0 or sv_host[-1] <= RANK_RTOL * sv_host[0]:
-        cond = float("inf") if sv_host[-1] == 0.0 else float(sv_host[0] / sv_host[-1])
+def pinv_dev(m_t: torch.Tensor, stream=None):
+    """pinv of M = m_t^T (k2 x k1) on the device (factor.py:112-130).
+    ``m_t``: k1 x k2 row-major fp64.  Returns (pinvT k2 x k1, stats[4]
+    device: sigma_max, sigma_min estimates, cond, singular flag); the caller
+    decides singularity after its one host sync.  One CTA of libsrlu
+    (Householder QR + rank test + R^-1 Q^T) when M fits in shared memory;
+    otherwise the QR comes from cuSOLVER and the rank test from libsrlu."""
+    L = _lib.lib()
+    m_t = m_t.contiguous()
+    k1, k2 = m_t.shape
+    if k2 < k1:
+        raise ShapeError(f"need rows >= cols, got {k2} x {k1}")
+    dev = m_t.device
+    stats = torch.empty(4, dtype=torch.float64, device=dev)
+    sh = _lib.stream_handle(stream)
+    if L.srlu_qr_pinv_smem_bytes(k1, k2) <= QR_SMEM_LIMIT:
+        pinv_t = torch.empty(k2, k1, dtype=torch.float64, device=dev)
+        _lib.check(L.srlu_qr_pinv(_lib.ptr(m_t), k1, k2, m_t.stride(0), _lib.ptr(pinv_t),
+                                  pinv_t.stride(0), _lib.ptr(stats), sh), "qr_pinv")
+        return pinv_t, stats
+    qf, rf = torch.linalg.qr(m_t.t(), mode="reduced")
+    rf = rf.contiguous()
+    _lib.check(L.srlu_rank_estimate(_lib.ptr(rf), k1, rf.stride(0), _lib.ptr(stats), sh),
+               "rank_estimate")
+    pinv_t = torch.linalg.solve_triangular(rf, qf.t().contiguous(), upper=True).t().contiguous()
+    return pinv_t, stats
+
+
+def dgemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    """out = a @ b (row-major fp64) with libsrlu's FMA GEMM."""
+    L = _lib.lib()
+    a = a if a.stride(1) == 1 else a.contiguous()
+    b = b if b.stride(1) == 1 else b.contiguous()
+    M, K = a.shape
+    K2, N = b.shape
+    if K != K2:
+        raise ShapeError(f"inner dimensions differ: {tuple(a.shape)} x {tuple(b.shape)}")
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.float64, device=a.device)
+    _lib.check(L.srlu_dgemm(_lib.ptr(a), a.stride(0), _lib.ptr(b), b.stride(0), _lib.ptr(out),
+                            out.stride(0), M, N, K, _lib.stream_handle(stream)), "dgemm")
+    return out
+
+
+def check_rank(stats_host):
+    """factor.py:123-128 on the estimates from pinv_dev."""
+    smax, smin, cond, singular = (float(x) for x in stats_host)
+    if singular:
+        cond = float("inf") if smin == 0.0 else float(smax / smin)
         raise SingularMatrixError(
             f"matrix is numerically rank deficient (condition estimate {cond:.3e})", cond=cond)
 
@@ -130,6 +168,6 @@ def left_pseudo_inverse(mat) -> Matrix:
     p, q = m.shape
     if p < q:
         raise ShapeError(f"need rows >= cols, got {p} x {q}")
-    pinv, sv = pinv_dev(m)
-    check_rank(sv.cpu().numpy())
-    return Matrix.from_device(pinv)
+    pinv_t, stats = pinv_dev(m.t().contiguous())
+    check_rank(stats.cpu().numpy())
+    return Matrix.from_device(pinv_t.t().contiguous())

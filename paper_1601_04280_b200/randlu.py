@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from .errors import DecompositionError, ParameterError, ShapeError, SingularMatrixError
-from .factor import RANK_RTOL, check_rank, lu_col_pivot_dev, lu_row_pivot_dev, pinv_dev
+from .factor import check_rank, dgemm, lu_col_pivot_dev, lu_row_pivot_dev, pinv_dev
 from .matrix import COMPLEX, REAL, Matrix, Permutation
 from .sketch import (HADAMARD, build_composite, members, sketch_left_into, sketch_right_into,
                      transform_kind_for_field)
@@ -223,30 +223,31 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
         sketch_left_into(a, om2, mrow, msign, bptr2, red_aT)
     ev[3].record()
 
-    pinv, sv = pinv_dev(red_lT.t())
-    core_t = red_aT @ pinv.t()          # (Omega2 P A)^T pinv^T = core^T, n x k1
+    pinv_t, stats = pinv_dev(red_lT)
+    core_t = dgemm(red_aT, pinv_t)      # (Omega2 P A)^T pinv^T = core^T, n x k1
     ev[4].record()
     core_keep = core_t.clone() if keep else None
 
     q, lt, ut = lu_col_pivot_dev(core_t)
-    l_final = l1 @ lt
+    l_final = dgemm(l1, lt)
     ev[5].record()
 
     # the one host sync of the attempt: rank test + non-finite flag
-    sv_host = sv.cpu().numpy()
+    stats_host = stats.cpu().numpy()
     fl = int(flag.item())
     if fl & 1:
         raise ValueError("matrix entries must be finite")
     if fl & 2:
         raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
-    check_rank(sv_host)
+    check_rank(stats_host)
     elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
     res = RandLuResult(P=Permutation(perm.cpu().numpy(), perm, validate=False),
                        Q=Permutation(q.cpu().numpy(), q, validate=False),
                        L=Matrix.from_device(l_final), U=_wrap(ut.t()), elapsed=elapsed,
                        attempt=attempt)
     if keep:
-        res.extras = dict(Y=y_keep, L1=l1, red_l=red_lT.t(), red_a=red_aT.t(), pinv=pinv,
+        res.extras = dict(Y=y_keep, L1=l1, red_l=red_lT.t(), red_a=red_aT.t(), pinv=pinv_t.t(),
+                          stats=stats_host,
                           core=core_keep.t(), Lt=lt, omega1=om1, omega2=om2)
     return res
 

@@ -13,6 +13,7 @@ import pytest
 
 from tests.conftest import cuda_ok
 from tests.golden import cases
+from tests.parity import check_tail
 
 pytestmark = pytest.mark.gpu
 
@@ -215,16 +216,14 @@ def test_pipeline_matches_reference(P, golden, name):
         np.testing.assert_array_equal(_np(ex["L1"]), g["L1"])
     np.testing.assert_array_equal(_np(ex["red_l"]), g["red_l"])
     np.testing.assert_array_equal(_np(ex["red_a"]), g["red_a"])
-    np.testing.assert_array_equal(res.Q.indices, g["Q"])
     assert _rel(_np(ex["core"]), g["core"]) <= 1e-12
-    assert _rel(res.L.numpy(), g["L"]) <= LU_RTOL
-    assert _rel(res.U.numpy(), g["U"]) <= LU_RTOL
+    l1 = g["L1"] if "L1" in g else _np(ex["L1"])
+    check_tail(res.Q.indices, res.L.numpy(), res.U.numpy(), g["Q"], g["L"], g["U"], g["core"],
+               g["red_l"], g["red_a"], l1)
     err = P.approximation_error(mat, res)
     want = float(g["err"])
-    if want == 0.0:
-        assert err == 0.0
-    else:
-        assert abs(err - want) <= 0.01 * want
+    anorm = np.linalg.norm(a.toarray() if hasattr(a, "toarray") else a)
+    assert abs(err - want) <= 0.01 * want + 1e-12 * anorm
     assert set(res.elapsed) == {"sketch1", "lu1", "sketch2", "pinv", "lu2", "total"}
 
 
@@ -295,6 +294,5 @@ def test_config2_full_size_vs_oracle(P):
     np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
     np.testing.assert_array_equal(res.P.indices, ref["P"])
     np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
-    np.testing.assert_array_equal(res.Q.indices, ref["Q"])
-    assert _rel(res.L.numpy(), ref["L"]) <= LU_RTOL
-    assert _rel(res.U.numpy(), ref["U"]) <= LU_RTOL
+    check_tail(res.Q.indices, res.L.numpy(), res.U.numpy(), ref["Q"], ref["L"], ref["U"],
+               ref["core"], ref["red_l"], ref["red_a"], ref["L1"])
