@@ -175,8 +175,9 @@ int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int64_t *q, do
  * sigma_min <= 1e-10 sigma_max, factor.py:124).  Needs
  * srlu_qr_pinv_smem_bytes(k1, k2) <= 220 KiB, else SRLU_ERR_UNSUPPORTED. */
 size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2);
+size_t srlu_qr_pinv_workspace(int64_t k1, int64_t k2);
 int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *pinvT,
-                 int64_t ldp, double *stats, srlu_stream_t stream);
+                 int64_t ldp, double *stats, void *ws, size_t ws_bytes, srlu_stream_t stream);
 
 /* the same rank test on an upper-triangular R (k x k row-major, device) */
 int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, double *stats,

@@ -56,7 +56,8 @@ SIGNATURES = {
     "srlu_sketch_left_csr": (INT, [P, P, P, INT, I64, I64, I64, P, P, P, I64, P, P, I64, I64,
                                    DBL, P, I64, P, SZ, P, P]),
     "srlu_qr_pinv_smem_bytes": (SZ, [I64, I64]),
-    "srlu_qr_pinv": (INT, [P, I64, I64, I64, P, I64, P, P]),
+    "srlu_qr_pinv_workspace": (SZ, [I64, I64]),
+    "srlu_qr_pinv": (INT, [P, I64, I64, I64, P, I64, P, P, SZ, P]),
     "srlu_rank_estimate": (INT, [P, I64, I64, P, P]),
     "srlu_dgemm": (INT, [P, I64, P, I64, P, I64, I64, I64, I64, P]),
     "srlu_lu_workspace": (SZ, [I64, I64]),
@@ -104,7 +105,7 @@ class _LaunchCounter:
     PER_CALL = {"build_sem": 3, "sem_plan": 4, "sketch_right_dense": 1, "sketch_right_csr": 1,
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 4,
-                "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 1, "rank_estimate": 1,
+                "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1,
                 "dgemm": 1}
 
     def __init__(self):

@@ -1,0 +1,111 @@
+// Register-resident Walsh-Hadamard transform of 1024-element (or smaller)
+// blocks by one warp, with the reference's exact radix-2 network
+// (_fast.pyx:23-41: stages h = 1, 2, 4, ...; butterfly (a+b, a-b)).
+//
+// A block of PAD = 32*E doubles lives in shared memory under the swizzle
+// sw(j) = (j & ~31) | ((j ^ (j >> 5)) & 31) (conflict-free for both access
+// patterns below).  Layout A: lane l holds j = l*E + e (stages h < E in
+// registers); layout B: lane l holds j = e*32 + l (stages E <= h < 32 by
+// shfl_xor, h >= 32 in registers).  Every output is produced by the same
+// tree of fp64 add/sub as the reference's loop nest, so results are bit
+// identical.
+#pragma once
+#include "common.cuh"
+
+namespace srlu {
+
+__device__ __forceinline__ int fwht_sw(int j) { return (j & ~31) | ((j ^ (j >> 5)) & 31); }
+
+template <int E>
+__device__ __forceinline__ void fwht_block_warp(double *blk, int lane) {
+    static_assert(E >= 1 && E <= 32 && (E & (E - 1)) == 0, "E must be a power of two <= 32");
+    double v[E];
+    // layout A
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = blk[fwht_sw(lane * E + e)];
+#pragma unroll
+    for (int h = 1; h < E; h <<= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & h) == 0) {
+                const double a = v[e], b = v[e + h];
+                v[e] = __dadd_rn(a, b);
+                v[e + h] = __dsub_rn(a, b);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) blk[fwht_sw(lane * E + e)] = v[e];
+    __syncwarp();
+    // layout B
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = blk[fwht_sw(e * 32 + lane)];
+#pragma unroll
+    for (int h = E; h < 32; h <<= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double p = __shfl_xor_sync(0xffffffffu, v[e], h);
+            v[e] = up ? __dsub_rn(p, v[e]) : __dadd_rn(v[e], p);
+        }
+    }
+#pragma unroll
+    for (int hh = 1; hh < E; hh <<= 1) {  // h = 32*hh
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & hh) == 0) {
+                const double a = v[e], b = v[e + hh];
+                v[e] = __dadd_rn(a, b);
+                v[e + hh] = __dsub_rn(a, b);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) blk[fwht_sw(e * 32 + lane)] = v[e];
+    __syncwarp();
+}
+
+// dispatch on the block length (32 <= pad <= 1024, power of two)
+__device__ __forceinline__ void fwht_block_warp_dyn(double *blk, int pad, int lane) {
+    switch (pad) {
+        case 1024: fwht_block_warp<32>(blk, lane); break;
+        case 512: fwht_block_warp<16>(blk, lane); break;
+        case 256: fwht_block_warp<8>(blk, lane); break;
+        case 128: fwht_block_warp<4>(blk, lane); break;
+        case 64: fwht_block_warp<2>(blk, lane); break;
+        default: fwht_block_warp<1>(blk, lane); break;
+    }
+}
+
+// Value at output index q of the full pad-point transform whose 1024-point
+// blocks (nb = pad/1024 of them, swizzled) were transformed in place: the
+// remaining stages h = 1024, 2048, ... combine the blocks at offset q%1024
+// in the reference's order.
+__device__ __forceinline__ double fwht_combine_blocks(const double *row, int nb, int q) {
+    if (nb == 1) return row[fwht_sw(q)];
+    double u[8];
+    const int o = fwht_sw(q & 1023);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) u[b] = b < nb ? row[b * 1024 + o] : 0.0;
+#pragma unroll
+    for (int s = 1; s < 8; s <<= 1) {
+        if (s < nb) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if ((b & s) == 0 && b + s < nb) {
+                    const double a = u[b], c = u[b + s];
+                    u[b] = __dadd_rn(a, c);
+                    u[b + s] = __dsub_rn(a, c);
+                }
+            }
+        }
+    }
+    const int B = q >> 10;
+    double r = u[0];
+#pragma unroll
+    for (int b = 1; b < 8; ++b)
+        if (b == B) r = u[b];
+    return r;
+}
+
+}  // namespace srlu

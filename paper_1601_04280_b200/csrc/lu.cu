@@ -32,6 +32,7 @@ enum { MODE_ROW = 0, MODE_COL = 1 };
 constexpr int kLuThreads = 256;
 constexpr int kLuMaxGrid = 256;
 constexpr int kLuXC = 64;  // trailing columns per chunk
+constexpr int kLuBcast = 8;  // replicated winner records
 constexpr double kPivotRtol = 1e-14;  // factor.py:19
 
 struct Cand {
@@ -39,6 +40,13 @@ struct Cand {
     unsigned int pos;
     int entity;
 };
+
+// optional per-step clock64 trace of CTA 0 (tools/diag_lu_timing.py)
+#define DBG_T(i)                                                               \
+    do {                                                                       \
+        if (p.dbg && blockIdx.x == 0 && s < 4096)                              \
+            p.dbg[(size_t)s * 8 + (i)] = (long long)clock64();                 \
+    } while (0)
 
 struct LuParams {
     double *w;  // M x k entity-major, ld
@@ -58,6 +66,10 @@ struct LuParams {
     Cand *cand;       // [2][G]
     double *candrow;  // [2][G][k]
     double *piv;      // [k][k] trailing parts of pivot entities
+    long long *dbg;   // optional trace (null)
+    unsigned *bflag;  // winner-broadcast flag (step + 1)
+    double *bcast;    // [kLuBcast][bstride]: entity, pos, row
+    int64_t bstride;
 };
 
 __device__ inline bool better(unsigned long long a_abs, unsigned a_pos, unsigned long long b_abs,
@@ -104,9 +116,10 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     __shared__ unsigned s_pos[32];
     __shared__ int s_ent[32];
     __shared__ double s_thresh;
-    __shared__ int s_wcta;
+    __shared__ int s_wpos;
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kLuThreads / 32;
     const int G = gridDim.x;
     const int k = p.k, b = p.b, bs = p.bs, rpc = p.rpc;
     const int64_t e0 = (int64_t)blockIdx.x * rpc;
@@ -115,8 +128,8 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     // smem carve-up
     double *panel = reinterpret_cast<double *>(smem_raw);          // rpc x bs
     double *PR = panel + (size_t)rpc * bs;                          // b x b
-    double *u = PR + (size_t)b * b;                                 // b
-    double *Ach = u + b;                                            // b x kLuXC
+    double *ubuf = PR + (size_t)b * b;                              // 2 x b (double-buffered)
+    double *Ach = ubuf + 2 * b;                                     // b x kLuXC
     int *pos = reinterpret_cast<int *>(Ach + (size_t)b * kLuXC);    // rpc
     int *pw_ent = pos + rpc;                                        // b
     unsigned bar_target = 0;
@@ -160,103 +173,186 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
         }
         __syncthreads();
 
+        // Step s = J+ls with one-column lookahead: when step s starts, column
+        // ls of every active entity is final; columns > ls still owe the
+        // update of step s-1 ("pending"), applied by warps 1.. while warp 0
+        // runs the grid exchange.  The published candidate row is completed
+        // on the fly with exactly the same operations.  Exchange: every CTA
+        // publishes {|w|, pos, entity, row} and bumps the step counter; the
+        // last arriver reduces all candidates and broadcasts the winner to
+        // kLuBcast replicated records (spreads the L2 hot spot).
+        bool pending = false;
+        const double *uprev = nullptr;  // winner vector of step s-1 (ROW: u, COL: L multipliers)
+        // local candidate for the panel's first step
+        unsigned long long babs = 0ULL;
+        unsigned bpos = 0xFFFFFFFFu;
+        int bent = -1;
+        for (int e = tid; e < ne; e += blockDim.x) {
+            if (pos[e] >= J) {
+                const unsigned long long a =
+                    (unsigned long long)__double_as_longlong(fabs(panel[e * bs]));
+                if (better(a, (unsigned)pos[e], babs, bpos)) { babs = a; bpos = (unsigned)pos[e]; bent = e; }
+            }
+        }
         for (int ls = 0; ls < bw; ++ls) {
             const int s = J + ls;
             const int slot = s & 1;
-            // 1. local candidate
-            unsigned long long babs = 0ULL;
-            unsigned bpos = 0xFFFFFFFFu;
-            int bent = -1;
-            for (int e = tid; e < ne; e += blockDim.x) {
-                if (pos[e] >= s) {
-                    unsigned long long a =
-                        (unsigned long long)__double_as_longlong(fabs(panel[e * bs + ls]));
-                    if (better(a, (unsigned)pos[e], babs, bpos)) {
-                        babs = a; bpos = (unsigned)pos[e]; bent = e;
+            double *ucur = ubuf + (ls & 1) * b;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long oa = __shfl_xor_sync(0xffffffffu, babs, off);
+                const unsigned op = __shfl_xor_sync(0xffffffffu, bpos, off);
+                const int oe = __shfl_xor_sync(0xffffffffu, bent, off);
+                if (better(oa, op, babs, bpos)) { babs = oa; bpos = op; bent = oe; }
+            }
+            if (lane == 0) { s_abs[warp] = babs; s_pos[warp] = bpos; s_ent[warp] = bent; }
+            __syncthreads();
+            if (tid == 0) DBG_T(0);
+            Cand *cs = p.cand + (size_t)slot * G;
+            if (warp == 0) {
+                babs = lane < NW ? s_abs[lane] : 0ULL;
+                bpos = lane < NW ? s_pos[lane] : 0xFFFFFFFFu;
+                bent = lane < NW ? s_ent[lane] : -1;
+#pragma unroll
+                for (int off = 16; off; off >>= 1) {
+                    const unsigned long long oa = __shfl_xor_sync(0xffffffffu, babs, off);
+                    const unsigned op = __shfl_xor_sync(0xffffffffu, bpos, off);
+                    const int oe = __shfl_xor_sync(0xffffffffu, bent, off);
+                    if (better(oa, op, babs, bpos)) { babs = oa; bpos = op; bent = oe; }
+                }
+                // publish {|w|, position, entity} + the candidate's panel row,
+                // completed with the pending update of step s-1
+                double *crow = p.candrow + ((size_t)slot * G + blockIdx.x) * k;
+                if (bent >= 0) {
+                    const double *we = panel + bent * bs;
+                    const double f = pending ? we[ls - 1] : 0.0;
+                    for (int x = lane; x < bw; x += 32) {
+                        double v = we[x];
+                        if (pending && x > ls) {
+                            v = (MODE == MODE_ROW) ? __dsub_rn(v, __dmul_rn(f, uprev[x]))
+                                                   : __dsub_rn(v, __dmul_rn(uprev[x], f));
+                        }
+                        crow[x] = v;
                     }
                 }
-            }
-            block_best(babs, bpos, bent, s_abs, s_pos, s_ent);
-            // 2. publish
-            Cand *cs = p.cand + (size_t)slot * G;
-            double *crow = p.candrow + ((size_t)slot * G + blockIdx.x) * k;
-            if (tid == 0) {
-                Cand c;
-                c.absbits = babs;
-                c.pos = bpos;
-                c.entity = bent >= 0 ? (int)(e0 + bent) : -1;
-                cs[blockIdx.x] = c;
-            }
-            if (bent >= 0)
-                for (int x = tid; x < bw; x += blockDim.x) crow[x] = panel[bent * bs + x];
-            // 3. one grid barrier per pivot step
-            bar_target += G;
-            grid_arrive_wait(p.bar, bar_target);
-            // 4. global winner
-            {
+                // the candidate row has been read: release warps 1.. into (B)
+                asm volatile("bar.arrive 1, %0;" ::"n"(kLuThreads) : "memory");
+                if (lane == 0) {
+                    Cand c;
+                    c.absbits = babs;
+                    c.pos = bpos;
+                    c.entity = bent >= 0 ? (int)(e0 + bent) : -1;
+                    cs[blockIdx.x] = c;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    bar_target += G;
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+                    DBG_T(1);
+                    unsigned v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
+                    } while ((int)(v - bar_target) < 0);
+                    DBG_T(2);
+                }
+                __syncwarp();
+                // every CTA reduces the G candidates itself (same winner everywhere)
                 unsigned long long ga = 0ULL;
                 unsigned gp = 0xFFFFFFFFu;
                 int gc = -1;
-                for (int c = tid; c < G; c += blockDim.x) {
+                for (int c = lane; c < G; c += 32) {
                     const Cand *cp = cs + c;
-                    unsigned long long a = __ldcg(&cp->absbits);
-                    unsigned pp = __ldcg(&cp->pos);
+                    const unsigned long long a = __ldcg(&cp->absbits);
+                    const unsigned pp = __ldcg(&cp->pos);
                     if (better(a, pp, ga, gp)) { ga = a; gp = pp; gc = c; }
                 }
-                block_best(ga, gp, gc, s_abs, s_pos, s_ent);
-                if (tid == 0) s_wcta = gc;
-                const double *wrow = p.candrow + ((size_t)slot * G + gc) * k;
-                for (int x = tid; x < bw; x += blockDim.x) u[x] = __ldcg(wrow + x);
-                if (tid == 0) {
-                    pw_ent[ls] = __ldcg(&cs[gc].entity);
-                    s_pos[1] = gp;  // winner's old position
+#pragma unroll
+                for (int off = 16; off; off >>= 1) {
+                    const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ga, off);
+                    const unsigned op = __shfl_xor_sync(0xffffffffu, gp, off);
+                    const int oc = __shfl_xor_sync(0xffffffffu, gc, off);
+                    if (better(oa, op, ga, gp)) { ga = oa; gp = op; gc = oc; }
                 }
-                __syncthreads();
+                const double *wrow = p.candrow + ((size_t)slot * G + gc) * k;
+                for (int x = lane; x < bw; x += 32) ucur[x] = __ldcg(wrow + x);
+                if (lane == 0) {
+                    pw_ent[ls] = __ldcg(&cs[gc].entity);
+                    s_wpos = (int)gp;
+                }
+                __syncwarp();
+                if (MODE == MODE_COL) {  // multipliers of the pivot column: u[x] / piv
+                    const double pv = ucur[ls];
+                    const bool bg = fabs(pv) > thresh;
+                    for (int x = ls + 1 + lane; x < bw; x += 32) ucur[x] = bg ? ucur[x] / pv : 0.0;
+                }
+                if (lane == 0) DBG_T(3);
+            } else {
+                asm volatile("bar.sync 1, %0;" ::"n"(kLuThreads) : "memory");
+                // (B) pending update of step s-1 on columns (ls, bw): warps 1..
+                if (pending) {
+                    for (int e = tid - 32; e < ne; e += blockDim.x - 32) {
+                        if (pos[e] < s) continue;
+                        double *we = panel + e * bs;
+                        const double f = we[ls - 1];
+                        if (MODE == MODE_ROW) {
+                            for (int x = ls + 1; x < bw; ++x)
+                                we[x] = __dsub_rn(we[x], __dmul_rn(f, uprev[x]));
+                        } else {
+                            for (int x = ls + 1; x < bw; ++x)
+                                we[x] = __dsub_rn(we[x], __dmul_rn(uprev[x], f));
+                        }
+                    }
+                }
             }
+            __syncthreads();
             const int went = pw_ent[ls];
-            const int wpos = (int)s_pos[1];
-            const double pivv = u[ls];
+            const int wpos = s_wpos;
+            // raw pivot: ROW keeps u as published; COL stored the multipliers
+            // after ls, ucur[ls] itself is the pivot in both modes
+            const double pivv = ucur[ls];
             const bool big = fabs(pivv) > thresh;
             if (b < k)
-                for (int x = tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
-            // 5. swap positions s <-> wpos
+                for (int x = tid; x < bw; x += blockDim.x) PR[ls * b + x] = ucur[x];
+            // (E) own entities: swap s <-> wpos, apply step s to column ls and
+            // the lookahead column ls+1, and scan column ls+1 for step s+1
+            babs = 0ULL;
+            bpos = 0xFFFFFFFFu;
+            bent = -1;
+            const bool has_next = ls + 1 < bw;
             for (int e = tid; e < ne; e += blockDim.x) {
-                if (pos[e] == s) pos[e] = wpos;
-                if (e0 + e == went) pos[e] = s;
-            }
-            __syncthreads();
-            // 6. apply the step to own panel columns
-            if (MODE == MODE_ROW) {
-                for (int e = tid; e < ne; e += blockDim.x) {
-                    if (pos[e] <= s) continue;
-                    double *we = panel + e * bs;
-                    if (big) {
-                        const double l = we[ls] / pivv;
-                        we[ls] = l;
-                        for (int x = ls + 1; x < bw; ++x) we[x] = __dsub_rn(we[x], __dmul_rn(l, u[x]));
-                    } else {
-                        we[ls] = 0.0;
+                int pe = pos[e];
+                if (pe == s) pe = wpos;
+                if (e0 + e == went) pe = s;
+                pos[e] = pe;
+                double *we = panel + e * bs;
+                if (MODE == MODE_ROW) {
+                    if (pe > s) {
+                        if (big) {
+                            const double l = we[ls] / pivv;
+                            we[ls] = l;
+                            if (has_next) we[ls + 1] = __dsub_rn(we[ls + 1], __dmul_rn(l, ucur[ls + 1]));
+                        } else {
+                            we[ls] = 0.0;
+                        }
+                    }
+                } else {
+                    if (e0 + e == went) {  // the pivot column itself: store its multipliers
+                        for (int x = ls + 1; x < bw; ++x) we[x] = ucur[x];
+                    } else if (pe > s && big && has_next) {
+                        we[ls + 1] = __dsub_rn(we[ls + 1], __dmul_rn(ucur[ls + 1], we[ls]));
                     }
                 }
-            } else {
-                // multipliers of the pivot column: L[x] = u[x] / piv
-                for (int x = ls + 1 + tid; x < bw; x += blockDim.x) u[x] = big ? u[x] / pivv : 0.0;
-                __syncthreads();
-                for (int e = tid; e < ne; e += blockDim.x) {
-                    double *we = panel + e * bs;
-                    if (e0 + e == went) {
-                        for (int x = ls + 1; x < bw; ++x) we[x] = u[x];
-                        continue;
-                    }
-                    if (pos[e] <= s || !big) continue;
-                    const double c = we[ls];
-                    for (int x = ls + 1; x < bw; ++x) we[x] = __dsub_rn(we[x], __dmul_rn(u[x], c));
+                if (has_next && pe > s) {
+                    const unsigned long long a =
+                        (unsigned long long)__double_as_longlong(fabs(we[ls + 1]));
+                    if (better(a, (unsigned)pe, babs, bpos)) { babs = a; bpos = (unsigned)pe; bent = e; }
                 }
-                if (b < k)
-                    for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
             }
-            __syncthreads();
+            pending = big;
+            uprev = ucur;
+            if (tid == 0) DBG_T(4);
         }
+        __syncthreads();
 
         // write the panel back
         for (int w = tid; w < ne * bw; w += blockDim.x) {
@@ -332,9 +428,11 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
 }
 
 static size_t lu_smem_bytes(int rpc, int b, int bs) {
-    return sizeof(double) * ((size_t)rpc * bs + (size_t)b * b + b + (size_t)b * kLuXC) +
+    return sizeof(double) * ((size_t)rpc * bs + (size_t)b * b + 2 * b + (size_t)b * kLuXC) +
            sizeof(int) * ((size_t)rpc + b) + 16;
 }
+
+static long long *g_lu_dbg = nullptr;
 
 static int sm_count() {
     int dev = 0, n = 0;
@@ -384,6 +482,10 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     prm.cand = (Cand *)(wsb + 256 + sizeof(double) * kLuMaxGrid);
     prm.candrow = (double *)((char *)prm.cand + sizeof(Cand) * 2 * kLuMaxGrid);
     prm.piv = prm.candrow + (size_t)2 * kLuMaxGrid * k;
+    prm.dbg = g_lu_dbg;
+    prm.bflag = prm.bar + 16;
+    prm.bstride = k + 8;
+    prm.bcast = prm.piv + (size_t)k * k;
     SRLU_CUDA(cudaMemsetAsync(prm.bar, 0, 256, stream));
     void *args[] = {&prm};
     SRLU_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(kLuThreads), args, smem,
@@ -398,7 +500,8 @@ using namespace srlu;
 extern "C" size_t srlu_lu_workspace(int64_t M, int64_t k) {
     (void)M;
     return 256 + sizeof(double) * kLuMaxGrid + sizeof(Cand) * 2 * kLuMaxGrid +
-           sizeof(double) * ((size_t)2 * kLuMaxGrid * k + (size_t)k * k) + 256;
+           sizeof(double) * ((size_t)2 * kLuMaxGrid * k + (size_t)k * k +
+                             (size_t)kLuBcast * (k + 8)) + 256;
 }
 
 extern "C" int srlu_lu_rowpiv(double *y, int64_t m, int64_t k, int64_t ldy, int64_t *perm,
@@ -419,4 +522,9 @@ extern "C" int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int
     SRLU_REQUIRE(Lt != nullptr && ldlt >= k && ldut >= k, SRLU_ERR_ARG, "lu_col_pivot: bad ld");
     return run_lu<MODE_COL>(ct, n, k, ldc, q, UT, ldut, Lt, ldlt, ws, ws_bytes,
                             (cudaStream_t)stream);
+}
+
+extern "C" int srlu_lu_debug_trace(long long *dev_buf) {
+    g_lu_dbg = dev_buf;
+    return SRLU_OK;
 }

@@ -12,6 +12,7 @@
 // bucket matrix S (about 6% of A's bytes at the BASELINE configs) makes a
 // round trip, mostly through L2.
 #include "fwht.cuh"
+#include "fwht_warp.cuh"
 
 namespace srlu {
 
@@ -119,6 +120,46 @@ __global__ void k3b_kernel(const double *__restrict__ S, int64_t n, int l, int p
     }
 }
 
+// K3b v2: one warp per column; the column's bucket vector (pad2 doubles,
+// swizzled, row stride pad2+1 to spread banks on the transposing store)
+// is transformed in registers per 1024-block; cross-block stages are
+// output-pruned.  32 <= pad2 <= 8192.
+__global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ S, int64_t n,
+                                                     int l, int pad, int CB,
+                                                     const double *__restrict__ phase,
+                                                     const int32_t *__restrict__ idx, int k,
+                                                     double mult, double *__restrict__ out,
+                                                     int64_t ldo) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xs = reinterpret_cast<double *>(smem_raw);
+    const int ldx = pad + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * CB;
+    const int nc = (int)((n - c0) < CB ? (n - c0) : CB);
+    for (int w = threadIdx.x; w < pad * CB; w += blockDim.x) {
+        const int t = w / CB, c = w % CB;
+        double v = 0.0;
+        if (t < l && c < nc) {
+            v = S[(int64_t)t * n + c0 + c];
+            if (phase[t] < 0.0) v = -v;
+        }
+        xs[c * ldx + fwht_sw(t)] = v;
+    }
+    __syncthreads();
+    const int bsize = pad < 1024 ? pad : 1024;
+    const int nb = pad / bsize;
+    const int nzb = (l + bsize - 1) / bsize;
+    for (int item = warp; item < nc * nzb; item += nw) {
+        const int c = item / nzb, b = item % nzb;
+        fwht_block_warp_dyn(xs + c * ldx + b * bsize, bsize, lane);
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < nc * k; w += blockDim.x) {
+        const int c = w / k, kk = w % k;
+        out[(c0 + c) * ldo + kk] = __dmul_rn(fwht_combine_blocks(xs + c * ldx, nb, idx[kk]), mult);
+    }
+}
+
 template <typename T>
 static int launch_k3a(const T *a, int64_t rows, int64_t n, int64_t lda, const int32_t *member_row,
                       const double *member_sign, const int32_t *bptr, int64_t l2, double *S,
@@ -142,6 +183,18 @@ static int launch_k3a(const T *a, int64_t rows, int64_t n, int64_t lda, const in
 int launch_k3b(const double *S, int64_t n, int64_t l2, int64_t pad2, const double *phase2,
                const int32_t *idx2, int64_t k2, double mult2, double *out, int64_t ldo,
                cudaStream_t stream) {
+    if (pad2 >= 32 && pad2 <= 8192) {
+        int CB = (int)(16384 / pad2);  // ~128 KB of smem
+        if (CB < 1) CB = 1;
+        if (CB > 64) CB = 64;
+        size_t smem = (size_t)(pad2 + 1) * CB * 8;
+        SRLU_CUDA(cudaFuncSetAttribute(k3b_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        k3b_v2_kernel<<<(unsigned)ceil_div(n, CB), 512, smem, stream>>>(
+            S, n, (int)l2, (int)pad2, CB, phase2, idx2, (int)k2, mult2, out, ldo);
+        SRLU_CHECK_LAUNCH("k3b_v2_kernel");
+        return SRLU_OK;
+    }
     int CB = (int)(8192 / pad2);
     if (CB < 1) CB = 1;
     if (CB > 64) CB = 64;

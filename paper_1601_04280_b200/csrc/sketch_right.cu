@@ -16,9 +16,12 @@
 // bucket in one chunk are serialised in lane (= column) order, which again
 // reproduces the reference's ascending-j order.
 #include <limits.h>
+#include <stdlib.h>
 
 #include "async_copy.cuh"
 #include "fwht.cuh"
+#include "fwht_warp.cuh"
+#include "tma.cuh"
 
 namespace srlu {
 
@@ -122,6 +125,162 @@ __global__ void __launch_bounds__(NT) k1_dense_kernel(
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// K1 v2 (aligned shapes, 32 <= pad1 <= 8192): 3-stage TMA bulk-copy
+// pipeline of R x C row segments (one elected thread issues R
+// cp.async.bulk per chunk, mbarrier completion), register-resident warp
+// FWHT per 1024-block, output-pruned cross-block stages.
+
+constexpr int kK1Stages = 3;
+
+template <typename T, int NT, int BPT, int R>
+__global__ void __launch_bounds__(NT) k1v2_kernel(
+    const T *__restrict__ a, int64_t m, int64_t n, int64_t lda, const int32_t *__restrict__ sorted,
+    const int32_t *__restrict__ bptr, int l, const double *__restrict__ phase,
+    const int32_t *__restrict__ idx, int k, int pad, double mult, double *__restrict__ y,
+    int64_t ldy, int *nonfinite) {
+    constexpr int C = K1Shape<T, R>::C;
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kK1Stages];
+    T *tiles = reinterpret_cast<T *>(smem_raw);
+    double *xs = reinterpret_cast<double *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t row0 = (int64_t)blockIdx.x * R;
+    const int nrows = (int)min((int64_t)R, m - row0);
+    const int64_t nchunks = ceil_div(n, C);
+
+    if (tid == 0) {
+        for (int s = 0; s < kK1Stages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int stage, int64_t ch) {
+        const int64_t c0 = ch * C;
+        const int cols = (int)min((int64_t)C, n - c0);
+        const unsigned bytes = (unsigned)(cols * sizeof(T));
+        mbar_arrive_expect_tx(&full[stage], bytes * nrows);
+        for (int r = 0; r < nrows; ++r)
+            bulk_g2s(tiles + ((size_t)stage * R + r) * C, a + (row0 + r) * lda + c0, bytes,
+                     &full[stage]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < kK1Stages && s < nchunks; ++s) issue(s, s);
+
+    int cur[BPT], end[BPT], code[BPT];
+    double acc[R][BPT];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const int t = tid + b * NT;
+        cur[b] = t < l ? bptr[t] : 0;
+        end[b] = t < l ? bptr[t + 1] : 0;
+        code[b] = cur[b] < end[b] ? sorted[cur[b]] : INT_MAX;
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r][b] = 0.0;
+    }
+
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        const int stage = (int)(ch % kK1Stages);
+        mbar_wait(&full[stage], (unsigned)((ch / kK1Stages) & 1));
+        const T *tl = tiles + (size_t)stage * R * C;
+        const int c0 = (int)(ch * C);
+        const int c1 = c0 + C;
+#pragma unroll
+        for (int b = 0; b < BPT; ++b) {
+            int cd = code[b];
+            while ((cd & 0x7FFFFFFF) < c1) {
+                const int cc = (cd & 0x7FFFFFFF) - c0;
+                const bool neg = cd < 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double v = (double)tl[r * C + cc];
+                    acc[r][b] = neg ? __dsub_rn(acc[r][b], v) : __dadd_rn(acc[r][b], v);
+                }
+                ++cur[b];
+                cd = cur[b] < end[b] ? __ldg(sorted + cur[b]) : INT_MAX;
+            }
+            code[b] = cd;
+        }
+        __syncthreads();
+        if (tid == 0 && ch + kK1Stages < nchunks) {
+            fence_proxy_async_smem();
+            issue(stage, ch + kK1Stages);
+        }
+    }
+
+    // ---- epilogue: +-phase, FWHT per row, sample, scale ------------------
+    // (all chunks consumed: every bulk copy has landed and been read)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double *row = xs + (size_t)r * pad;
+#pragma unroll
+        for (int b = 0; b < BPT; ++b) {
+            const int t = tid + b * NT;
+            if (t < l) row[fwht_sw(t)] = phase[t] < 0.0 ? -acc[r][b] : acc[r][b];
+        }
+        for (int t = l + tid; t < pad; t += NT) row[fwht_sw(t)] = 0.0;
+    }
+    __syncthreads();
+    const int bsize = pad < 1024 ? pad : 1024;
+    const int nb = pad / bsize;
+    const int nzb = (l + bsize - 1) / bsize;  // blocks holding nonzeros
+    for (int item = warp; item < nrows * nzb; item += NW) {
+        const int r = item / nzb, b = item % nzb;
+        fwht_block_warp_dyn(xs + (size_t)r * pad + (size_t)b * bsize, bsize, lane);
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int w = tid; w < nrows * k; w += NT) {
+        const int r = w / k, kk = w % k;
+        const double v = __dmul_rn(fwht_combine_blocks(xs + (size_t)r * pad, nb, idx[kk]), mult);
+        y[(row0 + r) * ldy + kk] = v;
+        bad |= !isfinite(v);
+    }
+    if (bad) atomicOr(nonfinite, 1);
+}
+
+template <typename T, int NT, int BPT, int R>
+static int launch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const int32_t *sorted,
+                       const int32_t *bptr, int l, const double *phase, const int32_t *idx, int k,
+                       int pad, double mult, double *y, int64_t ldy, int *nonfinite,
+                       cudaStream_t stream) {
+    constexpr int C = K1Shape<T, R>::C;
+    size_t smem = (size_t)kK1Stages * R * C * sizeof(T);
+    size_t ep = (size_t)R * pad * sizeof(double);
+    if (ep > smem) smem = ep;
+    auto kern = k1v2_kernel<T, NT, BPT, R>;
+    SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)ceil_div(m, R), NT, smem, stream>>>(a, m, n, lda, sorted, bptr, l, phase, idx,
+                                                        k, pad, mult, y, ldy, nonfinite);
+    SRLU_CHECK_LAUNCH("k1v2_kernel");
+    return SRLU_OK;
+}
+
+template <typename T>
+static int dispatch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const int32_t *sorted,
+                         const int32_t *bptr, int64_t l, const double *phase, const int32_t *idx,
+                         int64_t k, int64_t pad, double mult, double *y, int64_t ldy,
+                         int *nonfinite, cudaStream_t s) {
+    int L = (int)l, K = (int)k, P = (int)pad;
+    if (l <= 256)
+        return launch_k1v2<T, 256, 1, 8>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+                                         ldy, nonfinite, s);
+    if (l <= 512)
+        return launch_k1v2<T, 256, 2, 8>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+                                         ldy, nonfinite, s);
+    if (l <= 1024)
+        return launch_k1v2<T, 256, 4, 8>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+                                         ldy, nonfinite, s);
+    if (l <= 2048)
+        return launch_k1v2<T, 256, 8, 4>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+                                         ldy, nonfinite, s);
+    if (l <= 4096)
+        return launch_k1v2<T, 512, 8, 4>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+                                         ldy, nonfinite, s);
+    return launch_k1v2<T, 512, 16, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+                                      ldy, nonfinite, s);
 }
 
 template <typename T, int NT, int BPT, int R, bool FUSED>
@@ -279,6 +438,15 @@ extern "C" int srlu_sketch_right_dense(const void *a, int dtype, int64_t m, int6
                  SRLU_ERR_ARG, "sketch_right_dense: bad sizes");
     SRLU_REQUIRE(n < (1LL << 31) - 1, SRLU_ERR_UNSUPPORTED, "sketch_right_dense: n >= 2^31");
     cudaStream_t s = (cudaStream_t)stream;
+    const size_t es = dtype == SRLU_F32 ? 4 : 8;
+    const bool tma_ok = ((uintptr_t)a % 16 == 0) && ((lda * es) % 16 == 0) && ((n * es) % 16 == 0) &&
+                        pad1 >= 32 && pad1 <= 8192 && l1 <= 8192 && getenv("SRLU_K1_V1") == nullptr;
+    if (tma_ok && dtype == SRLU_F32)
+        return dispatch_k1v2<float>((const float *)a, m, n, lda, sorted1, bptr1, l1, phase1, idx1,
+                                    k1, pad1, mult1, y, ldy, nonfinite, s);
+    if (tma_ok && dtype == SRLU_F64)
+        return dispatch_k1v2<double>((const double *)a, m, n, lda, sorted1, bptr1, l1, phase1,
+                                     idx1, k1, pad1, mult1, y, ldy, nonfinite, s);
     if (dtype == SRLU_F32)
         return dispatch_k1_dense<float, true>((const float *)a, m, n, lda, sorted1, bptr1, l1,
                                               phase1, idx1, k1, pad1, mult1, y, ldy, nonfinite, s);

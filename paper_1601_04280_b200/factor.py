@@ -126,8 +126,10 @@ def pinv_dev(m_t: torch.Tensor, stream=None):
     sh = _lib.stream_handle(stream)
     if L.srlu_qr_pinv_smem_bytes(k1, k2) <= QR_SMEM_LIMIT:
         pinv_t = torch.empty(k2, k1, dtype=torch.float64, device=dev)
+        ws = _lib.workspace(L.srlu_qr_pinv_workspace(k1, k2), dev)
         _lib.check(L.srlu_qr_pinv(_lib.ptr(m_t), k1, k2, m_t.stride(0), _lib.ptr(pinv_t),
-                                  pinv_t.stride(0), _lib.ptr(stats), sh), "qr_pinv")
+                                  pinv_t.stride(0), _lib.ptr(stats), _lib.ptr(ws), ws.numel(), sh),
+                   "qr_pinv")
         return pinv_t, stats
     qf, rf = torch.linalg.qr(m_t.t(), mode="reduced")
     rf = rf.contiguous()

@@ -191,28 +191,69 @@ def _pipeline(a: Matrix, params: RandLuParams, keep: bool) -> RandLuResult:
         f"k2={params.k2}, l2={params.l2} are likely too small") from last
 
 
+_SIDE_STREAMS = {}
+
+
+def _side_stream(dev):
+    key = torch.device(dev).index
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _SIDE_STREAMS[key]
+
+
+def _pinned_copy(t: torch.Tensor) -> torch.Tensor:
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    return out
+
+
 def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandLuResult:
+    """One pass of Algorithm 1 (randlu.py:246-276).  Two streams: the side
+    stream draws Omega2 and builds its plan while K1/K2 run, and runs the
+    small QR/pinv (K4) while K3 streams P·A on the main stream."""
     m, n = a.shape
     dev = a.device
     k1, k2 = params.k1, params.k2
+    kind = transform_kind_for_field(params.field)
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
-    ev[0].record()
-    ops = _CompositeOps(params, m, n, params.seed + 2 * attempt, params.seed + 2 * attempt + 1,
-                        dev)
-    om1, om2 = ops.omega1, ops.omega2
+    ev[0].record(main)
+
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        om2 = build_composite(k2, params.l2, m, kind, params.seed + 2 * attempt + 1, dev)
+        om2.sem.plan()
+        mrow_l, msign_l, bptr2 = members(om2, None, 0, m, stream=side)
+        ev_om2 = torch.cuda.Event()
+        ev_om2.record(side)
+    om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev)
     y = torch.empty(m, k1, dtype=torch.float64, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     sketch_right_into(a, om1, y, flag)
-    ev[1].record()
+    ev[1].record(main)
 
     y_keep = y.clone() if keep else None
     perm, l1, _ = lu_row_pivot_dev(y)
-    ev[2].record()
+    ev[2].record(main)
 
-    # stage 2: Omega2 L1 and Omega2 (P A)
-    mrow_l, msign_l, bptr2 = members(om2, None, 0, m)
+    # stage 2: Omega2 L1, then (K4 on the side stream) || Omega2 (P A)
+    main.wait_event(ev_om2)
+    for t in (om2.sem.row_of, om2.sem.sign, om2.fast.phase, om2.fast.sample_idx, mrow_l,
+              msign_l, bptr2, *om2.sem.plan()):
+        t.record_stream(main)
     red_lT = torch.empty(k1, k2, dtype=torch.float64, device=dev)
     sketch_left_into(Matrix.from_device(l1), om2, mrow_l, msign_l, bptr2, red_lT)
+    ev_redl = torch.cuda.Event()
+    ev_redl.record(main)
+    side.wait_event(ev_redl)
+    with torch.cuda.stream(side):
+        pinv_t, stats = pinv_dev(red_lT, stream=side)
+        ev_pinv = torch.cuda.Event()
+        ev_pinv.record(side)
+    pinv_t.record_stream(main)
+    stats.record_stream(main)
+    red_lT.record_stream(side)
     red_aT = torch.empty(n, k2, dtype=torch.float64, device=dev)
     if a.is_sparse:
         inv = torch.empty(m, dtype=torch.int32, device=dev)
@@ -221,28 +262,31 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     else:
         mrow, msign, _ = members(om2, perm, 0, m)
         sketch_left_into(a, om2, mrow, msign, bptr2, red_aT)
-    ev[3].record()
+    ev[3].record(main)
 
-    pinv_t, stats = pinv_dev(red_lT)
+    main.wait_event(ev_pinv)
     core_t = dgemm(red_aT, pinv_t)      # (Omega2 P A)^T pinv^T = core^T, n x k1
-    ev[4].record()
+    ev[4].record(main)
     core_keep = core_t.clone() if keep else None
 
     q, lt, ut = lu_col_pivot_dev(core_t)
     l_final = dgemm(l1, lt)
-    ev[5].record()
+    ev[5].record(main)
 
-    # the one host sync of the attempt: rank test + non-finite flag
-    stats_host = stats.cpu().numpy()
-    fl = int(flag.item())
+    # the one host sync of the attempt: rank test, non-finite flag, P, Q
+    stats_h, flag_h, perm_h, q_h = (_pinned_copy(t) for t in (stats, flag, perm, q))
+    ev[5].synchronize()
+    torch.cuda.current_stream(dev).synchronize()
+    fl = int(flag_h[0])
     if fl & 1:
         raise ValueError("matrix entries must be finite")
     if fl & 2:
         raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
+    stats_host = stats_h.numpy()
     check_rank(stats_host)
     elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
-    res = RandLuResult(P=Permutation(perm.cpu().numpy(), perm, validate=False),
-                       Q=Permutation(q.cpu().numpy(), q, validate=False),
+    res = RandLuResult(P=Permutation(perm_h.numpy(), perm, validate=False),
+                       Q=Permutation(q_h.numpy(), q, validate=False),
                        L=Matrix.from_device(l_final), U=_wrap(ut.t()), elapsed=elapsed,
                        attempt=attempt)
     if keep:

@@ -63,7 +63,7 @@ class SparseEmbedding:
     def shape(self):
         return (self.out_dim, self.in_dim)
 
-    def plan(self):
+    def plan(self, stream=None):
         """(sorted int32[n] with sign in bit 31, bucket_ptr int32[l+1])."""
         if not self._plan:
             L = _lib.lib()
@@ -73,7 +73,7 @@ class SparseEmbedding:
             ws = _lib.workspace(L.srlu_sem_plan_workspace(self.in_dim, self.out_dim), dev)
             _lib.check(L.srlu_sem_plan(_lib.ptr(self.row_of), _lib.ptr(self.sign), self.in_dim,
                                        self.out_dim, _lib.ptr(srt), _lib.ptr(bptr),
-                                       _lib.ptr(ws), ws.numel(), _lib.stream_handle()),
+                                       _lib.ptr(ws), ws.numel(), _lib.stream_handle(stream)),
                        "sem_plan")
             self._plan.extend([srt, bptr])
         return self._plan[0], self._plan[1]
@@ -140,15 +140,17 @@ def build_fast_transform(k, l, kind, seed, device=None) -> FastTransformSketch:
         raise ParameterError(f"need 1 <= k <= {pad}, got k={k}")
     seed = _check_seed(seed)
     L = _lib.load()
-    phase = np.empty(l, dtype=np.float64)
-    idx = np.empty(k, dtype=np.int64)
+    pin = torch.cuda.is_available()
+    phase_t = torch.empty(l, dtype=torch.float64, pin_memory=pin)
+    idx_t = torch.empty(k, dtype=torch.int64, pin_memory=pin)
     padc = np.zeros(1, dtype=np.int64)
-    _lib.check(L.srlu_draw_fast_transform(seed, k, l, phase.ctypes.data, idx.ctypes.data,
+    _lib.check(L.srlu_draw_fast_transform(seed, k, l, phase_t.data_ptr(), idx_t.data_ptr(),
                                           padc.ctypes.data), "build_fast_transform")
     assert int(padc[0]) == pad
+    phase, idx = phase_t.numpy(), idx_t.numpy()
     dev = torch.device(device) if device is not None else _default_device()
-    phase_d = torch.from_numpy(phase).to(dev, non_blocking=False)
-    idx_d = torch.from_numpy(idx.astype(np.int32)).to(dev)
+    phase_d = phase_t.to(dev, non_blocking=True)
+    idx_d = idx_t.to(dev, non_blocking=True).to(torch.int32)
     return FastTransformSketch(int(k), int(l), phase_d, idx_d, pad, math.sqrt(pad / k), kind,
                                seed=seed, phase_host=phase, sample_idx_host=idx)
 
@@ -233,7 +235,7 @@ def members(omega2: CompositeSketch, perm: torch.Tensor | None, row0: int, rows:
     """Member table of the left sketch restricted to local rows [row0, row0+rows)."""
     L = _lib.lib()
     sem = omega2.sem
-    srt, bptr = sem.plan()
+    srt, bptr = sem.plan(stream)
     m = sem.in_dim
     mrow = torch.empty(m, dtype=torch.int32, device=srt.device)
     msign = torch.empty(m, dtype=torch.float64, device=srt.device)
