@@ -3,8 +3,8 @@
 // (_fast.pyx:23-41: stages h = 1, 2, 4, ...; butterfly (a+b, a-b)).
 //
 // A block of PAD = 32*E doubles lives in shared memory under the swizzle
-// sw(j) = (j & ~31) | ((j ^ (j >> 5)) & 31) (conflict-free for both access
-// patterns below).  Layout A: lane l holds j = l*E + e (stages h < E in
+// sw(j) = (j & ~31) | ((j & 31) ^ ((j >> 5) & 15)) (at most the minimal 2
+// wavefronts per 8-byte access for both access patterns below).  Layout A: lane l holds j = l*E + e (stages h < E in
 // registers); layout B: lane l holds j = e*32 + l (stages E <= h < 32 by
 // shfl_xor, h >= 32 in registers).  Every output is produced by the same
 // tree of fp64 add/sub as the reference's loop nest, so results are bit
@@ -14,7 +14,8 @@
 
 namespace srlu {
 
-__device__ __forceinline__ int fwht_sw(int j) { return (j & ~31) | ((j ^ (j >> 5)) & 31); }
+// XOR the lane bits with bits 5..8 only: block-local for any block >= 512
+__device__ __forceinline__ int fwht_sw(int j) { return (j & ~31) | ((j & 31) ^ ((j >> 5) & 15)); }
 
 template <int E>
 __device__ __forceinline__ void fwht_block_warp(double *blk, int lane) {
@@ -77,21 +78,32 @@ __device__ __forceinline__ void fwht_block_warp_dyn(double *blk, int pad, int la
     }
 }
 
-// Value at output index q of the full pad-point transform whose 1024-point
-// blocks (nb = pad/1024 of them, swizzled) were transformed in place: the
-// remaining stages h = 1024, 2048, ... combine the blocks at offset q%1024
-// in the reference's order.
-__device__ __forceinline__ double fwht_combine_blocks(const double *row, int nb, int q) {
+// same for blocks of at most 512 points (16 registers per lane)
+__device__ __forceinline__ void fwht_block_warp_dyn512(double *blk, int pad, int lane) {
+    switch (pad) {
+        case 512: fwht_block_warp<16>(blk, lane); break;
+        case 256: fwht_block_warp<8>(blk, lane); break;
+        case 128: fwht_block_warp<4>(blk, lane); break;
+        case 64: fwht_block_warp<2>(blk, lane); break;
+        default: fwht_block_warp<1>(blk, lane); break;
+    }
+}
+
+// Value at output index q of the full pad-point transform whose bsize-point
+// blocks (nb = pad/bsize <= 16 of them, swizzled) were transformed in
+// place: the remaining stages h = bsize, 2*bsize, ... combine the blocks at
+// offset q % bsize in the reference's order.
+__device__ __forceinline__ double fwht_combine_blocks(const double *row, int bsize, int nb, int q) {
     if (nb == 1) return row[fwht_sw(q)];
-    double u[8];
-    const int o = fwht_sw(q & 1023);
+    double u[16];
+    const int o = fwht_sw(q & (bsize - 1));
 #pragma unroll
-    for (int b = 0; b < 8; ++b) u[b] = b < nb ? row[b * 1024 + o] : 0.0;
+    for (int b = 0; b < 16; ++b) u[b] = b < nb ? row[b * bsize + o] : 0.0;
 #pragma unroll
-    for (int s = 1; s < 8; s <<= 1) {
+    for (int s = 1; s < 16; s <<= 1) {
         if (s < nb) {
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
+            for (int b = 0; b < 16; ++b) {
                 if ((b & s) == 0 && b + s < nb) {
                     const double a = u[b], c = u[b + s];
                     u[b] = __dadd_rn(a, c);
@@ -100,10 +112,10 @@ __device__ __forceinline__ double fwht_combine_blocks(const double *row, int nb,
             }
         }
     }
-    const int B = q >> 10;
+    const int B = q / bsize;
     double r = u[0];
 #pragma unroll
-    for (int b = 1; b < 8; ++b)
+    for (int b = 1; b < 16; ++b)
         if (b == B) r = u[b];
     return r;
 }

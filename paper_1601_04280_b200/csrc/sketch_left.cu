@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ 
     }
     __syncthreads();
     const int bsize = pad < 1024 ? pad : 1024;
-    const int nb = pad / bsize;
+    const int nb = pad / bsize;  // <= 8 for pad2 <= 8192
     const int nzb = (l + bsize - 1) / bsize;
     for (int item = warp; item < nc * nzb; item += nw) {
         const int c = item / nzb, b = item % nzb;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ 
     __syncthreads();
     for (int w = threadIdx.x; w < nc * k; w += blockDim.x) {
         const int c = w / k, kk = w % k;
-        out[(c0 + c) * ldo + kk] = __dmul_rn(fwht_combine_blocks(xs + c * ldx, nb, idx[kk]), mult);
+        out[(c0 + c) * ldo + kk] = __dmul_rn(fwht_combine_blocks(xs + c * ldx, bsize, nb, idx[kk]), mult);
     }
 }
 

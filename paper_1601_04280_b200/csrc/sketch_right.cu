@@ -133,7 +133,12 @@ __global__ void __launch_bounds__(NT) k1_dense_kernel(
 // cp.async.bulk per chunk, mbarrier completion), register-resident warp
 // FWHT per 1024-block, output-pruned cross-block stages.
 
-constexpr int kK1Stages = 3;
+constexpr int kK1Stages = 2;
+
+template <typename T, int R>
+struct K1v2Shape {
+    static constexpr int C = 65536 / (R * (int)sizeof(T));  // 64 KB per stage
+};
 
 template <typename T, int NT, int BPT, int R>
 __global__ void __launch_bounds__(NT) k1v2_kernel(
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
     const int32_t *__restrict__ bptr, int l, const double *__restrict__ phase,
     const int32_t *__restrict__ idx, int k, int pad, double mult, double *__restrict__ y,
     int64_t ldy, int *nonfinite) {
-    constexpr int C = K1Shape<T, R>::C;
+    constexpr int C = K1v2Shape<T, R>::C;
     constexpr int NW = NT / 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kK1Stages];
@@ -223,18 +228,19 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
         for (int t = l + tid; t < pad; t += NT) row[fwht_sw(t)] = 0.0;
     }
     __syncthreads();
-    const int bsize = pad < 1024 ? pad : 1024;
+    const int bsize = pad < 512 ? pad : 512;  // 16 values per lane in registers
     const int nb = pad / bsize;
     const int nzb = (l + bsize - 1) / bsize;  // blocks holding nonzeros
     for (int item = warp; item < nrows * nzb; item += NW) {
         const int r = item / nzb, b = item % nzb;
-        fwht_block_warp_dyn(xs + (size_t)r * pad + (size_t)b * bsize, bsize, lane);
+        fwht_block_warp_dyn512(xs + (size_t)r * pad + (size_t)b * bsize, bsize, lane);
     }
     __syncthreads();
     bool bad = false;
     for (int w = tid; w < nrows * k; w += NT) {
         const int r = w / k, kk = w % k;
-        const double v = __dmul_rn(fwht_combine_blocks(xs + (size_t)r * pad, nb, idx[kk]), mult);
+        const double v =
+            __dmul_rn(fwht_combine_blocks(xs + (size_t)r * pad, bsize, nb, idx[kk]), mult);
         y[(row0 + r) * ldy + kk] = v;
         bad |= !isfinite(v);
     }
@@ -246,7 +252,7 @@ static int launch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const int3
                        const int32_t *bptr, int l, const double *phase, const int32_t *idx, int k,
                        int pad, double mult, double *y, int64_t ldy, int *nonfinite,
                        cudaStream_t stream) {
-    constexpr int C = K1Shape<T, R>::C;
+    constexpr int C = K1v2Shape<T, R>::C;
     size_t smem = (size_t)kK1Stages * R * C * sizeof(T);
     size_t ep = (size_t)R * pad * sizeof(double);
     if (ep > smem) smem = ep;
@@ -264,22 +270,18 @@ static int dispatch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const in
                          int64_t k, int64_t pad, double mult, double *y, int64_t ldy,
                          int *nonfinite, cudaStream_t s) {
     int L = (int)l, K = (int)k, P = (int)pad;
-    if (l <= 256)
-        return launch_k1v2<T, 256, 1, 8>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
-                                         ldy, nonfinite, s);
-    if (l <= 512)
-        return launch_k1v2<T, 256, 2, 8>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
-                                         ldy, nonfinite, s);
+    // one thread per bucket (1024 threads), 64 KB row-segment chunks
     if (l <= 1024)
-        return launch_k1v2<T, 256, 4, 8>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
-                                         ldy, nonfinite, s);
+        return launch_k1v2<T, 1024, 1, (sizeof(T) == 4 ? 4 : 2)>(a, m, n, lda, sorted, bptr, L,
+                                                                   phase, idx, K, P, mult, y, ldy,
+                                                                   nonfinite, s);
     if (l <= 2048)
-        return launch_k1v2<T, 256, 8, 4>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
-                                         ldy, nonfinite, s);
+        return launch_k1v2<T, 1024, 2, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult,
+                                          y, ldy, nonfinite, s);
     if (l <= 4096)
-        return launch_k1v2<T, 512, 8, 4>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
-                                         ldy, nonfinite, s);
-    return launch_k1v2<T, 512, 16, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
+        return launch_k1v2<T, 1024, 4, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult,
+                                          y, ldy, nonfinite, s);
+    return launch_k1v2<T, 1024, 8, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
                                       ldy, nonfinite, s);
 }
 

@@ -220,18 +220,19 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
     ev[0].record(main)
 
-    side.wait_stream(main)
+    om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev)
+    y = torch.empty(m, k1, dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    sketch_right_into(a, om1, y, flag)
+    ev[1].record(main)
+    # Omega2 (draws + plan + member table of L1) on the side stream while K1
+    # runs (independent of everything enqueued so far)
     with torch.cuda.stream(side):
         om2 = build_composite(k2, params.l2, m, kind, params.seed + 2 * attempt + 1, dev)
         om2.sem.plan()
         mrow_l, msign_l, bptr2 = members(om2, None, 0, m, stream=side)
         ev_om2 = torch.cuda.Event()
         ev_om2.record(side)
-    om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev)
-    y = torch.empty(m, k1, dtype=torch.float64, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    sketch_right_into(a, om1, y, flag)
-    ev[1].record(main)
 
     y_keep = y.clone() if keep else None
     perm, l1, _ = lu_row_pivot_dev(y)

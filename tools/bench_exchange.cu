@@ -6,6 +6,79 @@
 
 struct Cand { unsigned long long absbits; unsigned pos; int entity; };
 
+template <int R>
+__global__ void xchg12_kernel(unsigned *counter, Cand *cand, double *rows, int rounds, int k,
+                              unsigned long long *out, double *sink) {
+    const int G = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned target = 0;
+    __shared__ double u[2][640];
+    long long t0 = clock64();
+    unsigned long long seed = blockIdx.x * 2654435761ull;
+    const int my = blockIdx.x % R;
+    for (int r = 0; r < rounds; ++r) {
+        const int slot = r & 1;
+        if (warp == 0) {
+            for (int rep = 0; rep < R; ++rep) {
+                double *crow = rows + (((size_t)rep * 2 + slot) * G + blockIdx.x) * k;
+                for (int x = lane; x < k; x += 32) crow[x] = (double)(r + x);
+            }
+            if (lane < R) {
+                seed = seed * 6364136223846793005ull + 1442695040888963407ull;
+                Cand c; c.absbits = (seed >> 12) + r; c.pos = blockIdx.x; c.entity = blockIdx.x;
+                cand[((size_t)lane * 2 + slot) * G + blockIdx.x] = c;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                target += G;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+                unsigned v;
+                do { asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory"); }
+                while ((int)(v - target) < 0);
+            }
+            __syncwarp();
+            unsigned long long ga = 0; unsigned gp = 0xffffffffu; int gc = 0;
+            for (int c = lane; c < G; c += 32) {
+                const Cand *cp = cand + ((size_t)my * 2 + slot) * G + c;
+                unsigned long long a = __ldcg(&cp->absbits); unsigned pp = __ldcg(&cp->pos);
+                if (a > ga || (a == ga && pp < gp)) { ga = a; gp = pp; gc = c; }
+            }
+            for (int off = 16; off; off >>= 1) {
+                unsigned long long oa = __shfl_xor_sync(0xffffffffu, ga, off);
+                unsigned op = __shfl_xor_sync(0xffffffffu, gp, off);
+                int oc = __shfl_xor_sync(0xffffffffu, gc, off);
+                if (oa > ga || (oa == ga && op < gp)) { ga = oa; gp = op; gc = oc; }
+            }
+            const double *wrow = rows + (((size_t)my * 2 + slot) * G + gc) * k;
+            for (int x = lane; x < k; x += 32) u[slot][x] = __ldcg(wrow + x);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) u[slot][0] += 1.0;
+        __syncthreads();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) sink[blockIdx.x] = u[0][0];
+    if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+}
+
+template <int R>
+void run12(int G, int rounds, int k) {
+    unsigned *counter; Cand *cand; double *rows, *sink; unsigned long long *out;
+    cudaMalloc(&counter, 4); cudaMalloc(&cand, sizeof(Cand) * 2 * G * R);
+    cudaMalloc(&rows, 8 * 2 * (size_t)G * k * R); cudaMalloc(&out, 8); cudaMalloc(&sink, 8 * G);
+    cudaMemset(counter, 0, 4);
+    void *args[] = {&counter, &cand, &rows, &rounds, &k, &out, &sink};
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel((void *)xchg12_kernel<R>, G, 256, args, 0, 0);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    unsigned long long cyc; cudaMemcpy(&cyc, out, 8, cudaMemcpyDeviceToHost);
+    printf("variant 12 R=%d G=%d k=%d: %.3f us/round (%.0f cyc) %s\n", R, G, k, ms * 1e3 / rounds,
+           (double)cyc / rounds, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(counter); cudaFree(cand); cudaFree(rows); cudaFree(out); cudaFree(sink);
+}
+
 template <int V>
 __global__ void xchg_kernel(unsigned *counter, Cand *cand, double *rows, int rounds, int k,
                             unsigned long long *out, double *sink) {
@@ -166,7 +239,7 @@ void run(int G, int rounds, int k) {
 }
 
 int main() {
-    run<1>(148, 2000, 110); run11(148, 2000, 110); run11(148, 2000, 550); run11(74, 2000, 110);
-    run11(8, 2000, 110);
+    run<1>(148, 2000, 110); run12<1>(148, 2000, 110); run12<4>(148, 2000, 110); run12<8>(148, 2000, 110);
+    run12<16>(148, 2000, 110); run12<8>(148, 2000, 550);
     return 0;
 }
