@@ -277,6 +277,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--dist", action="store_true",
+                    help="use the row-sharded path even at world size 1 (NCCL)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -293,8 +295,11 @@ def main():
         return run_reference_arm(args, cfg, metric, workload)
 
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0",
+                              WORLD_SIZE="1", LOCAL_RANK="0")
         dist.init_process_group("nccl")
         from paper_1601_04280_b200 import dist as D
         return D.bench_main(args, cfg, metric, workload, gen_config, time_region, flush_l2,
