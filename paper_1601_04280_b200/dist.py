@@ -18,7 +18,7 @@ split into contiguous row shards; rank g owns rows [row0_g, row0_g+rows_g).
            decision is broadcast so all ranks retry in lockstep.
 
 The per-rank compute is an injectable ``ops`` object: ``CudaOps`` (libsrlu
-kernels, the product path) or, in tests, a CPU stand-in built on the oracle
+kernels, the product path) or, in tests, a numpy CPU stand-in
 (tests/test_dist_gloo.py) — the sharding/collective logic is the same code.
 """
 
