@@ -156,32 +156,44 @@ size_t srlu_lu_workspace(int64_t M, int64_t k);
  * perm[m] (position -> row), L (m x k row-major, position order, unit
  * lower-trapezoidal), U (k x k row-major, may be NULL). */
 int srlu_lu_rowpiv(double *y, int64_t m, int64_t k, int64_t ldy, int64_t *perm, double *L,
-                   int64_t ldl, double *U, int64_t ldu, void *ws, size_t ws_bytes,
-                   srlu_stream_t stream);
+                   int64_t ldl, double *U, int64_t ldu, int reserve_sms, void *ws,
+                   size_t ws_bytes, srlu_stream_t stream);
+
+/* Both LUs are one cooperative persistent kernel, one CTA per SM;
+ * `reserve_sms` SMs are left out of the grid so a kernel already running on
+ * another stream (the rank test, srlu_qr_rank) does not hold the launch
+ * back.  0 = use every SM. */
 
 /* Column-pivoted LU of core (k x n) given as its transpose ct (n x k
  * row-major, overwritten): q[n], Lt (k x k row-major unit lower),
  * UT (n x k row-major) = U^T, i.e. U (k x n) in column-major storage. */
 int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int64_t *q, double *Lt,
-                   int64_t ldlt, double *UT, int64_t ldut, void *ws, size_t ws_bytes,
-                   srlu_stream_t stream);
+                   int64_t ldlt, double *UT, int64_t ldut, int reserve_sms, void *ws,
+                   size_t ws_bytes, srlu_stream_t stream);
 
 /* ---- small dense tail (K4) --------------------------------------------- */
 
 /* left_pseudo_inverse (factor.py:112-130) of M (k2 x k1) given as mT = M^T
  * (k1 x k2 row-major), in one CTA: Householder QR, rank test, and
- * pinvT = (R^-1 Q^T)^T (k2 x k1 row-major).  stats[4] (device):
- * sigma_max estimate, sigma_min estimate, cond, singular flag (1.0 when
- * sigma_min <= 1e-10 sigma_max, factor.py:124).  Needs
+ * pinvT = (R^-1 Q^T)^T (k2 x k1 row-major); the rank test is
+ * srlu_qr_rank (stats[4]: sigma_max estimate, sigma_min estimate, cond,
+ * singular flag = 1.0 when sigma_min <= 1e-10 sigma_max, factor.py:124).
+ * `stats` is unused here (kept for ABI stability).  Needs
  * srlu_qr_pinv_smem_bytes(k1, k2) <= 220 KiB, else SRLU_ERR_UNSUPPORTED. */
 size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2);
 size_t srlu_qr_pinv_workspace(int64_t k1, int64_t k2);
 int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *pinvT,
                  int64_t ldp, double *stats, void *ws, size_t ws_bytes, srlu_stream_t stream);
 
-/* the same rank test on an upper-triangular R (k x k row-major, device) */
-int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, double *stats,
-                       srlu_stream_t stream);
+/* the rank test on the R left in the srlu_qr_pinv workspace `ws` (run it
+ * after srlu_qr_pinv on the same stream; it can overlap later work on
+ * other streams: only the host's final decision needs stats). */
+int srlu_qr_rank(const void *ws, int64_t k1, int64_t k2, double *stats, srlu_stream_t stream);
+
+/* the same rank test on an upper-triangular R (k x k, k <= 576, device),
+ * given row-major (R, ldr) and transposed (RT = R^T row-major, ldt) */
+int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, const double *RT, int64_t ldt,
+                       double *stats, srlu_stream_t stream);
 
 /* C (M x N) = A (M x K) · B (K x N), row-major fp64 (matrix.py:219-230 matmul
  * for randlu.py:267 and :272) */

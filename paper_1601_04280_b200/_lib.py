@@ -58,11 +58,12 @@ SIGNATURES = {
     "srlu_qr_pinv_smem_bytes": (SZ, [I64, I64]),
     "srlu_qr_pinv_workspace": (SZ, [I64, I64]),
     "srlu_qr_pinv": (INT, [P, I64, I64, I64, P, I64, P, P, SZ, P]),
-    "srlu_rank_estimate": (INT, [P, I64, I64, P, P]),
+    "srlu_rank_estimate": (INT, [P, I64, I64, P, I64, P, P]),
+    "srlu_qr_rank": (INT, [P, I64, I64, P, P]),
     "srlu_dgemm": (INT, [P, I64, P, I64, P, I64, I64, I64, I64, P]),
     "srlu_lu_workspace": (SZ, [I64, I64]),
-    "srlu_lu_rowpiv": (INT, [P, I64, I64, I64, P, P, I64, P, I64, P, SZ, P]),
-    "srlu_lu_colpiv": (INT, [P, I64, I64, I64, P, P, I64, P, I64, P, SZ, P]),
+    "srlu_lu_rowpiv": (INT, [P, I64, I64, I64, P, P, I64, P, I64, INT, P, SZ, P]),
+    "srlu_lu_colpiv": (INT, [P, I64, I64, I64, P, P, I64, P, I64, INT, P, SZ, P]),
 }
 
 _lib = None
@@ -105,7 +106,7 @@ class _LaunchCounter:
     PER_CALL = {"build_sem": 3, "sem_plan": 4, "sketch_right_dense": 1, "sketch_right_csr": 1,
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 4,
-                "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1,
+                "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1,
                 "dgemm": 1}
 
     def __init__(self):

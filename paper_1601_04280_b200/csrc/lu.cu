@@ -345,13 +345,15 @@ static int sm_count() {
 
 template <int MODE>
 static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, double *out_main,
-                  int64_t ld_main, double *out_small, int64_t ld_small, void *ws,
-                  size_t ws_bytes, cudaStream_t stream) {
+                  int64_t ld_main, double *out_small, int64_t ld_small, int reserve_sms,
+                  void *ws, size_t ws_bytes, cudaStream_t stream) {
     SRLU_REQUIRE(M >= 1 && k >= 1 && ld >= k, SRLU_ERR_ARG, "lu: bad sizes M=%lld k=%lld",
                  (long long)M, (long long)k);
     SRLU_REQUIRE(M < (1LL << 31) - 1 && k <= 8192, SRLU_ERR_UNSUPPORTED, "lu: sizes too large");
     SRLU_REQUIRE(ws_bytes >= srlu_lu_workspace(M, k), SRLU_ERR_WORKSPACE, "lu: workspace too small");
-    int G = sm_count();
+    SRLU_REQUIRE(reserve_sms >= 0, SRLU_ERR_ARG, "lu: reserve_sms < 0");
+    int G = sm_count() - reserve_sms;
+    if (G < 1) G = 1;
     if (const char *env = getenv("SRLU_LU_MAX_GRID")) {  // testing knob
         int cap = atoi(env);
         if (cap >= 1 && cap < G) G = cap;
@@ -402,21 +404,21 @@ extern "C" size_t srlu_lu_workspace(int64_t M, int64_t k) {
 }
 
 extern "C" int srlu_lu_rowpiv(double *y, int64_t m, int64_t k, int64_t ldy, int64_t *perm,
-                              double *L, int64_t ldl, double *U, int64_t ldu, void *ws,
-                              size_t ws_bytes, srlu_stream_t stream) {
+                              double *L, int64_t ldl, double *U, int64_t ldu, int reserve_sms,
+                              void *ws, size_t ws_bytes, srlu_stream_t stream) {
     SRLU_REQUIRE(m >= k, SRLU_ERR_ARG, "lu_row_pivot: need rows >= cols, got %lld x %lld",
                  (long long)m, (long long)k);
     SRLU_REQUIRE(ldl >= k && (U == nullptr || ldu >= k), SRLU_ERR_ARG, "lu_row_pivot: bad ld");
-    return run_lu<MODE_ROW>(y, m, k, ldy, perm, L, ldl, U, ldu, ws, ws_bytes,
+    return run_lu<MODE_ROW>(y, m, k, ldy, perm, L, ldl, U, ldu, reserve_sms, ws, ws_bytes,
                             (cudaStream_t)stream);
 }
 
 extern "C" int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int64_t *q,
-                              double *Lt, int64_t ldlt, double *UT, int64_t ldut, void *ws,
-                              size_t ws_bytes, srlu_stream_t stream) {
+                              double *Lt, int64_t ldlt, double *UT, int64_t ldut, int reserve_sms,
+                              void *ws, size_t ws_bytes, srlu_stream_t stream) {
     SRLU_REQUIRE(k <= n, SRLU_ERR_ARG, "lu_col_pivot: need rows <= cols, got %lld x %lld",
                  (long long)k, (long long)n);
     SRLU_REQUIRE(Lt != nullptr && ldlt >= k && ldut >= k, SRLU_ERR_ARG, "lu_col_pivot: bad ld");
-    return run_lu<MODE_COL>(ct, n, k, ldc, q, UT, ldut, Lt, ldlt, ws, ws_bytes,
+    return run_lu<MODE_COL>(ct, n, k, ldc, q, UT, ldut, Lt, ldlt, reserve_sms, ws, ws_bytes,
                             (cudaStream_t)stream);
 }

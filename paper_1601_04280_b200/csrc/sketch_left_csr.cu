@@ -11,6 +11,7 @@
 // +-phase, the radix-2 FWHT over pad2 and the k2-row subsample, and writes
 // row j of (Omega2 P A)^T.  P·A is never formed.
 #include "fwht.cuh"
+#include "fwht_warp.cuh"
 
 namespace srlu {
 
@@ -86,25 +87,31 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
     }
 }
 
-__global__ void csr_col_project_kernel(const int64_t *__restrict__ colptr,
-                                       const unsigned long long *__restrict__ keys,
-                                       const double *__restrict__ ev, int64_t n, int l, int pad,
-                                       const double *__restrict__ phase,
-                                       const int32_t *__restrict__ idx, int k, double mult,
-                                       double *__restrict__ out, int64_t ldo, int *flags) {
+// One CTA per column (grid-stride); handles columns with lo < count <= CAP.
+template <int CAP>
+__global__ void __launch_bounds__(256) csr_col_project_kernel(
+    const int64_t *__restrict__ colptr, const unsigned long long *__restrict__ keys,
+    const double *__restrict__ ev, int64_t n, int l, int pad, const double *__restrict__ phase,
+    const int32_t *__restrict__ idx, int k, double mult, double *__restrict__ out, int64_t ldo,
+    int *flags, int lo) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *x = reinterpret_cast<double *>(smem_raw);                    // pad
-    unsigned long long *sk = reinterpret_cast<unsigned long long *>(x + pad);  // cap
-    double *sv = reinterpret_cast<double *>(sk + kCsrColCap);            // cap
+    double *x = reinterpret_cast<double *>(smem_raw);                          // pad
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(x + pad);  // CAP
+    double *sv = reinterpret_cast<double *>(sk + CAP);                         // CAP
+    const bool reg = pad >= 32;
+    const int bsize = pad < 512 ? pad : 512;
+    const int nb = pad / bsize;
+    const int nzb = (l + bsize - 1) / bsize;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
         const int64_t p0 = colptr[j];
         const int cnt = (int)(colptr[j + 1] - p0);
-        for (int t = threadIdx.x; t < pad; t += blockDim.x) x[t] = 0.0;
-        if (cnt > kCsrColCap) {
-            if (threadIdx.x == 0) atomicOr(flags, 2);
-            __syncthreads();
+        if (cnt <= lo) continue;  // handled by the smaller-capacity launch (uniform)
+        if (cnt > CAP) {  // longer columns: next launch, or unsupported in the last one
+            if (flags != nullptr && threadIdx.x == 0) atomicOr(flags, 2);
             continue;
         }
+        for (int t = threadIdx.x; t < pad; t += blockDim.x) x[t] = 0.0;
         int n2 = 1;
         while (n2 < cnt) n2 <<= 1;
         for (int i = threadIdx.x; i < n2; i += blockDim.x) {
@@ -123,11 +130,11 @@ __global__ void csr_col_project_kernel(const int64_t *__restrict__ colptr,
                     const int ixj = i ^ jj;
                     if (ixj > i) {
                         const bool up = (i & kk) == 0;
-                        unsigned long long a = sk[i], b = sk[ixj];
+                        const unsigned long long a = sk[i], b = sk[ixj];
                         if ((a > b) == up) {
                             sk[i] = b;
                             sk[ixj] = a;
-                            double tv = sv[i];
+                            const double tv = sv[i];
                             sv[i] = sv[ixj];
                             sv[ixj] = tv;
                         }
@@ -142,12 +149,20 @@ __global__ void csr_col_project_kernel(const int64_t *__restrict__ colptr,
             if (i > 0 && (unsigned)(sk[i - 1] >> 32) == t) continue;
             double acc = 0.0;
             for (int e = i; e < cnt && (unsigned)(sk[e] >> 32) == t; ++e) acc = __dadd_rn(acc, sv[e]);
-            x[t] = phase[t] < 0.0 ? -acc : acc;
+            x[reg ? fwht_sw((int)t) : (int)t] = phase[t] < 0.0 ? -acc : acc;
         }
         __syncthreads();
-        fwht_smem_cta(x, pad);
-        for (int kk = threadIdx.x; kk < k; kk += blockDim.x)
-            out[j * ldo + kk] = __dmul_rn(x[idx[kk]], mult);
+        if (reg) {
+            for (int b = warp; b < nzb; b += blockDim.x >> 5)
+                fwht_block_warp_dyn512(x + b * bsize, bsize, lane);
+            __syncthreads();
+        } else {
+            fwht_smem_cta(x, pad);
+        }
+        for (int kk = threadIdx.x; kk < k; kk += blockDim.x) {
+            const double fv = reg ? fwht_combine_blocks(x, bsize, nb, idx[kk]) : x[idx[kk]];
+            out[j * ldo + kk] = __dmul_rn(fv, mult);
+        }
         __syncthreads();
     }
 }
@@ -200,14 +215,27 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
                                                            w.keys, w.ev);
         SRLU_CHECK_LAUNCH("csr_fill_kernel");
     }
-    size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * kCsrColCap;
-    SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left_csr: pad2 too large");
-    SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int64_t grid = n < 148 * 8 ? n : 148 * 8;
-    csr_col_project_kernel<<<(unsigned)grid, 256, smem, s>>>(w.colptr, w.keys, w.ev, n, (int)l2,
-                                                             (int)pad2, phase2, idx2, (int)k2,
-                                                             mult2, out, ldo, flags);
+    // columns with <= 2048 entries: small smem, high occupancy; longer ones
+    // (<= 8192) in a second launch; longer still -> flags |= 2
+    const int64_t grid = n < 148 * 16 ? n : 148 * 16;
+    {
+        size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * 2048;
+        SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel<2048>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        csr_col_project_kernel<2048><<<(unsigned)grid, 256, smem, s>>>(
+            w.colptr, w.keys, w.ev, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
+            nullptr, -1);
+        SRLU_CHECK_LAUNCH("csr_col_project_kernel<2048>");
+    }
+    {
+        size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * kCsrColCap;
+        SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left_csr: pad2 too large");
+        SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel<kCsrColCap>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        csr_col_project_kernel<kCsrColCap><<<(unsigned)(grid < 148 ? grid : 148), 256, smem, s>>>(
+            w.colptr, w.keys, w.ev, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
+            flags, 2048);
+    }
     SRLU_CHECK_LAUNCH("csr_col_project_kernel");
     return SRLU_OK;
 }

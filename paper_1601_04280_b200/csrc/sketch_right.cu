@@ -247,6 +247,157 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
     if (bad) atomicOr(nonfinite, 1);
 }
 
+// ---------------------------------------------------------------------------
+// K1 v3: persistent (grid = #SMs); each CTA walks its row blocks (R rows)
+// and their 1-D chunks as ONE item stream through a kK1Stages-deep TMA
+// bulk-copy ring, so the loads of the next row block are in flight while
+// the current block's FWHT epilogue runs (separate epilogue buffer).
+
+template <typename T, int NT, int BPT, int R>
+__global__ void __launch_bounds__(NT, 1) k1v3_kernel(
+    const T *__restrict__ a, int64_t m, int64_t n, int64_t lda, const int32_t *__restrict__ sorted,
+    const int32_t *__restrict__ bptr, int l, const double *__restrict__ phase,
+    const int32_t *__restrict__ idx, int k, int pad, double mult, double *__restrict__ y,
+    int64_t ldy, int *nonfinite, int C) {
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kK1Stages];
+    T *tiles = reinterpret_cast<T *>(smem_raw);
+    double *xs = reinterpret_cast<double *>(smem_raw + (size_t)kK1Stages * R * C * sizeof(T));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nrb = ceil_div(m, R);
+    const int64_t nchunks = ceil_div(n, C);
+    const int64_t my_rb = nrb > blockIdx.x ? ceil_div(nrb - blockIdx.x, gridDim.x) : 0;
+    const int64_t nitems = my_rb * nchunks;
+
+    if (tid == 0) {
+        for (int st = 0; st < kK1Stages; ++st) mbar_init(&full[st], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t it) {
+        const int stage = (int)(it % kK1Stages);
+        const int64_t rb = blockIdx.x + (it / nchunks) * gridDim.x;
+        const int64_t ch = it % nchunks;
+        const int64_t row0 = rb * R;
+        const int nrows = (int)min((int64_t)R, m - row0);
+        const int64_t c0 = ch * C;
+        const int cols = (int)min((int64_t)C, n - c0);
+        const unsigned bytes = (unsigned)(cols * sizeof(T));
+        mbar_arrive_expect_tx(&full[stage], bytes * nrows);
+        for (int r = 0; r < nrows; ++r)
+            bulk_g2s(tiles + ((size_t)stage * R + r) * C, a + (row0 + r) * lda + c0, bytes,
+                     &full[stage]);
+    };
+    if (tid == 0)
+        for (int64_t it = 0; it < kK1Stages && it < nitems; ++it) issue(it);
+
+    int cur[BPT], end[BPT], code[BPT];
+    double acc[R][BPT];
+    bool bad = false;
+    for (int64_t it = 0; it < nitems; ++it) {
+        const int stage = (int)(it % kK1Stages);
+        const int64_t ch = it % nchunks;
+        const int64_t rb = blockIdx.x + (it / nchunks) * gridDim.x;
+        if (ch == 0) {
+#pragma unroll
+            for (int b = 0; b < BPT; ++b) {
+                const int t = tid + b * NT;
+                cur[b] = t < l ? bptr[t] : 0;
+                end[b] = t < l ? bptr[t + 1] : 0;
+                code[b] = cur[b] < end[b] ? __ldg(sorted + cur[b]) : INT_MAX;
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r][b] = 0.0;
+            }
+        }
+        mbar_wait(&full[stage], (unsigned)((it / kK1Stages) & 1));
+        const T *tl = tiles + (size_t)stage * R * C;
+        const int c0 = (int)(ch * C);
+        const int c1 = c0 + C;
+#pragma unroll
+        for (int b = 0; b < BPT; ++b) {
+            int cd = code[b];
+            while ((cd & 0x7FFFFFFF) < c1) {
+                const int cc = (cd & 0x7FFFFFFF) - c0;
+                const bool neg = cd < 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double v = (double)tl[r * C + cc];
+                    acc[r][b] = neg ? __dsub_rn(acc[r][b], v) : __dadd_rn(acc[r][b], v);
+                }
+                ++cur[b];
+                cd = cur[b] < end[b] ? __ldg(sorted + cur[b]) : INT_MAX;
+            }
+            code[b] = cd;
+        }
+        __syncthreads();  // stage consumed by everyone
+        if (tid == 0 && it + kK1Stages < nitems) {
+            fence_proxy_async_smem();
+            issue(it + kK1Stages);
+        }
+        if (ch == nchunks - 1) {
+            // epilogue for row block rb: +-phase, FWHT, sample, scale
+            const int64_t row0 = rb * R;
+            const int nrows = (int)min((int64_t)R, m - row0);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double *row = xs + (size_t)r * pad;
+#pragma unroll
+                for (int b = 0; b < BPT; ++b) {
+                    const int t = tid + b * NT;
+                    if (t < l) row[fwht_sw(t)] = phase[t] < 0.0 ? -acc[r][b] : acc[r][b];
+                }
+                for (int t = l + tid; t < pad; t += NT) row[fwht_sw(t)] = 0.0;
+            }
+            __syncthreads();
+            const int bsize = pad < 512 ? pad : 512;
+            const int nb = pad / bsize;
+            const int nzb = (l + bsize - 1) / bsize;
+            for (int item = warp; item < nrows * nzb; item += NW) {
+                const int r = item / nzb, b = item % nzb;
+                fwht_block_warp_dyn512(xs + (size_t)r * pad + (size_t)b * bsize, bsize, lane);
+            }
+            __syncthreads();
+            for (int w = tid; w < nrows * k; w += NT) {
+                const int r = w / k, kk = w % k;
+                const double v =
+                    __dmul_rn(fwht_combine_blocks(xs + (size_t)r * pad, bsize, nb, idx[kk]), mult);
+                y[(row0 + r) * ldy + kk] = v;
+                bad |= !isfinite(v);
+            }
+            __syncthreads();  // xs reused by the next block
+        }
+    }
+    if (bad) atomicOr(nonfinite, 1);
+}
+
+template <typename T, int NT, int BPT, int R>
+static int launch_k1v3(const T *a, int64_t m, int64_t n, int64_t lda, const int32_t *sorted,
+                       const int32_t *bptr, int l, const double *phase, const int32_t *idx, int k,
+                       int pad, double mult, double *y, int64_t ldy, int *nonfinite,
+                       cudaStream_t stream) {
+    const size_t xs_bytes = (size_t)R * pad * sizeof(double);
+    const size_t budget = 200 * 1024;
+    size_t stage = 64 * 1024;
+    if (kK1Stages * stage + xs_bytes > budget) stage = (budget - xs_bytes) / kK1Stages;
+    int C = (int)(stage / (R * sizeof(T)));
+    C &= ~127;  // multiple of 128 elements (16-byte bulk copies)
+    if ((int64_t)C > n) C = (int)((n + 3) & ~3LL);
+    if (C < 128) C = 128;
+    const size_t smem = (size_t)kK1Stages * R * C * sizeof(T) + xs_bytes;
+    auto kern = k1v3_kernel<T, NT, BPT, R>;
+    SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nrb = ceil_div(m, R);
+    const unsigned grid = (unsigned)(nrb < sms ? nrb : sms);
+    kern<<<grid, NT, smem, stream>>>(a, m, n, lda, sorted, bptr, l, phase, idx, k, pad, mult, y,
+                                     ldy, nonfinite, C);
+    SRLU_CHECK_LAUNCH("k1v3_kernel");
+    return SRLU_OK;
+}
+
 template <typename T, int NT, int BPT, int R>
 static int launch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const int32_t *sorted,
                        const int32_t *bptr, int l, const double *phase, const int32_t *idx, int k,
@@ -270,7 +421,23 @@ static int dispatch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const in
                          int64_t k, int64_t pad, double mult, double *y, int64_t ldy,
                          int *nonfinite, cudaStream_t s) {
     int L = (int)l, K = (int)k, P = (int)pad;
-    // one thread per bucket (1024 threads), 64 KB row-segment chunks
+    // persistent grid, TMA ring, 512 threads (128 registers: no spills)
+    if (getenv("SRLU_K1_V3") != nullptr) {  // experimental persistent variant (slower today)
+        if (l <= 512)
+            return launch_k1v3<T, 512, 1, (sizeof(T) == 4 ? 4 : 2)>(
+                a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y, ldy, nonfinite, s);
+        if (l <= 1024)
+            return launch_k1v3<T, 512, 2, (sizeof(T) == 4 ? 4 : 2)>(
+                a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y, ldy, nonfinite, s);
+        if (l <= 2048)
+            return launch_k1v3<T, 512, 4, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P,
+                                             mult, y, ldy, nonfinite, s);
+        if (l <= 4096)
+            return launch_k1v3<T, 512, 8, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P,
+                                             mult, y, ldy, nonfinite, s);
+        return launch_k1v3<T, 512, 16, 1>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult,
+                                          y, ldy, nonfinite, s);
+    }
     if (l <= 1024)
         return launch_k1v2<T, 1024, 1, (sizeof(T) == 4 ? 4 : 2)>(a, m, n, lda, sorted, bptr, L,
                                                                    phase, idx, K, P, mult, y, ldy,
@@ -344,6 +511,12 @@ __global__ void __launch_bounds__(WPB * 32) k1_csr_kernel(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *x = reinterpret_cast<double *>(smem_raw) + (size_t)warp * pad;
+    // register FWHT (512-point blocks, swizzled) when pad >= 32
+    const bool reg = pad >= 32;
+    auto P = [&](int t) { return reg ? fwht_sw(t) : t; };
+    const int bsize = pad < 512 ? pad : 512;
+    const int nb = pad / bsize;
+    const int nzb = (l + bsize - 1) / bsize;
     bool bad = false;
     for (int64_t row = (int64_t)blockIdx.x * WPB + warp; row < m; row += (int64_t)gridDim.x * WPB) {
         for (int t = lane; t < pad; t += 32) x[t] = 0.0;
@@ -364,22 +537,27 @@ __global__ void __launch_bounds__(WPB * 32) k1_csr_kernel(
             unsigned peers = 0;
             if (valid) peers = __match_any_sync(active, t);
             const bool uniq = valid && peers == (1u << lane);
-            if (uniq) x[t] = __dadd_rn(x[t], val);
+            if (uniq) x[P(t)] = __dadd_rn(x[P(t)], val);
             unsigned conflict = __ballot_sync(0xffffffffu, valid && !uniq);
             while (conflict) {  // same bucket twice in this chunk: ascending column order
                 const int src = __ffs(conflict) - 1;
-                if (lane == src) x[t] = __dadd_rn(x[t], val);
+                if (lane == src) x[P(t)] = __dadd_rn(x[P(t)], val);
                 __syncwarp();
                 conflict &= conflict - 1;
             }
             __syncwarp();
         }
         for (int t = lane; t < l; t += 32)
-            if (phase[t] < 0.0) x[t] = -x[t];
+            if (phase[t] < 0.0) x[P(t)] = -x[P(t)];
         __syncwarp();
-        fwht_smem_warp(x, pad, lane);
+        if (reg) {
+            for (int b = 0; b < nzb; ++b) fwht_block_warp_dyn512(x + b * bsize, bsize, lane);
+        } else {
+            fwht_smem_warp(x, pad, lane);
+        }
         for (int kk = lane; kk < k; kk += 32) {
-            double v = __dmul_rn(x[idx[kk]], mult);
+            const double fv = reg ? fwht_combine_blocks(x, bsize, nb, idx[kk]) : x[idx[kk]];
+            const double v = __dmul_rn(fv, mult);
             y[row * ldy + kk] = v;
             bad |= !isfinite(v);
         }

@@ -65,26 +65,116 @@ __device__ inline double block_min(double v, double *red) {
     return s;
 }
 
-// R accessor: upper triangle R(r, c), r <= c
-struct RSmem {  // column-major with stride ld (the QR workspace)
-    const double *a;
-    int ld;
-    __device__ double operator()(int r, int c) const { return a[c * ld + r]; }
-};
-struct RGlobalRowMajor {
-    const double *a;
-    int64_t ld;
-    __device__ double operator()(int r, int c) const { return a[(int64_t)r * ld + c]; }
-};
+// Rank test on an upper-triangular R given twice: Rr (row-major, row r
+// contiguous) and Rc (column-major, column c contiguous).  stats[0] =
+// sigma_max estimate, [1] = sigma_min estimate, [2] = cond, [3] = singular.
+//  * sigma_max >= max(|R_jj|, ||R x||) over 6 power iterations (whole CTA);
+//  * sigma_min <= min(|R_jj|, ||(R^T R)^-1 x||^-1/2) over 3 inverse
+//    iterations.  The two triangular solves run on warp 0 in axpy form with
+//    the vector distributed over the lanes' registers (lane l owns entries
+//    j == l mod 32) and the next row/column prefetched, so each of the k
+//    sequential steps costs one shuffle broadcast + k/32 FMAs.
+constexpr int kRankMaxPerLane = 18;  // k <= 576
 
-// stats[0] = sigma_max estimate, [1] = sigma_min estimate, [2] = cond, [3] = singular flag
-template <typename RA>
-__device__ void rank_estimate(RA R, int k, double *x, double *y, double *rinv, double *red,
-                              double *stats) {
+// warp 0: 3 inverse iterations, vectors distributed over lane registers
+// (lane l owns entries j == l mod 32, PER per lane), next row prefetched.
+template <int PER>
+__device__ double inverse_iteration(const double *__restrict__ Rr, int64_t ldr,
+                                    const double *__restrict__ Rc, int64_t ldc, int k,
+                                    double est, double inv_sqrt_k) {
+    const int lane = threadIdx.x & 31;
+    double v[PER], rd[PER], w[PER], nx[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int j = i * 32 + lane;
+        v[i] = j < k ? ((j & 1) ? -inv_sqrt_k : inv_sqrt_k) : 0.0;
+        rd[i] = j < k ? 1.0 / Rr[(int64_t)j * ldr + j] : 0.0;
+        w[i] = 0.0;
+    }
+    for (int it = 0; it < 3; ++it) {
+        // R^T w = v (forward, axpy form on rows of R)
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int c = i * 32 + lane;
+            nx[i] = c < k ? Rr[c] : 0.0;  // row 0
+        }
+        for (int r = 0; r < k; ++r) {
+            double cur[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) cur[i] = nx[i];
+            if (r + 1 < k) {
+                const double *nrow = Rr + (int64_t)(r + 1) * ldr;
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int c = i * 32 + lane;
+                    nx[i] = c < k ? nrow[c] : 0.0;
+                }
+            }
+            const int ro = r & 31, ri = r >> 5;
+            double vr = 0.0, rdr = 0.0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i)
+                if (i == ri) { vr = v[i]; rdr = rd[i]; }
+            const double wr = __shfl_sync(0xffffffffu, vr * rdr, ro);
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int c = i * 32 + lane;
+                if (c > r) v[i] = __fma_rn(-cur[i], wr, v[i]);
+                if (i == ri && lane == ro) w[i] = wr;
+            }
+        }
+        // R z = w (backward, axpy form on columns of R = rows of Rc)
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int r = i * 32 + lane;
+            nx[i] = r < k ? Rc[(int64_t)(k - 1) * ldc + r] : 0.0;
+        }
+        for (int c = k - 1; c >= 0; --c) {
+            double cur[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) cur[i] = nx[i];
+            if (c > 0) {
+                const double *ncol = Rc + (int64_t)(c - 1) * ldc;
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int r = i * 32 + lane;
+                    nx[i] = r < c - 1 ? ncol[r] : 0.0;
+                }
+            }
+            const int co = c & 31, ci = c >> 5;
+            double wc = 0.0, rdc = 0.0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i)
+                if (i == ci) { wc = w[i]; rdc = rd[i]; }
+            const double zc = __shfl_sync(0xffffffffu, wc * rdc, co);
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int r = i * 32 + lane;
+                if (r < c) w[i] = __fma_rn(-cur[i], zc, w[i]);
+                if (i == ci && lane == co) v[i] = zc;
+            }
+        }
+        double zz = 0.0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) zz = __fma_rn(v[i], v[i], zz);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, off);
+        if (!(zz > 0.0) || !isfinite(zz)) return 0.0;
+        est = fmin(est, 1.0 / sqrt(sqrt(zz)));
+        const double inv = 1.0 / sqrt(zz);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) v[i] *= inv;
+    }
+    return est;
+}
+
+__device__ void rank_estimate(const double *__restrict__ Rr, int64_t ldr,
+                              const double *__restrict__ Rc, int64_t ldc, int k, double *x,
+                              double *y, double *red, double *stats) {
     const int tid = threadIdx.x;
     double dmax = 0.0, dmin = INFINITY;
     for (int j = tid; j < k; j += blockDim.x) {
-        double d = fabs(R(j, j));
+        const double d = fabs(Rr[(int64_t)j * ldr + j]);
         dmax = fmax(dmax, d);
         dmin = fmin(dmin, d);
     }
@@ -92,73 +182,47 @@ __device__ void rank_estimate(RA R, int k, double *x, double *y, double *rinv, d
     dmin = block_min(dmin, red);
     double smax = dmax, smin = dmin;
     const double inv_sqrt_k = 1.0 / sqrt((double)k);
-    // power iteration: sigma_max >= ||R x|| for unit x
     for (int j = tid; j < k; j += blockDim.x) x[j] = inv_sqrt_k;
     __syncthreads();
     for (int it = 0; it < 6 && dmax > 0.0; ++it) {
         double ss = 0.0;
-        for (int r = tid; r < k; r += blockDim.x) {
-            double s = 0.0;
-            for (int c = r; c < k; ++c) s += R(r, c) * x[c];
-            y[r] = s;
-            ss += s * s;
+        for (int r = tid; r < k; r += blockDim.x) {  // y = R x (row r of R)
+            const double *row = Rr + (int64_t)r * ldr;
+            double s0 = 0.0, s1 = 0.0;
+            int c = r;
+            for (; c + 1 < k; c += 2) {
+                s0 += row[c] * x[c];
+                s1 += row[c + 1] * x[c + 1];
+            }
+            if (c < k) s0 += row[c] * x[c];
+            y[r] = s0 + s1;
+            ss += (s0 + s1) * (s0 + s1);
         }
         ss = block_sum(ss, red);
         smax = fmax(smax, sqrt(ss));
         double zz = 0.0;
-        for (int c = tid; c < k; c += blockDim.x) {
-            double s = 0.0;
-            for (int r = 0; r <= c; ++r) s += R(r, c) * y[r];
-            x[c] = s;  // y is complete (synced by block_sum)
-            zz += s * s;
+        for (int c = tid; c < k; c += blockDim.x) {  // x = R^T y (column c of R)
+            const double *col = Rc + (int64_t)c * ldc;
+            double s0 = 0.0, s1 = 0.0;
+            int r = 0;
+            for (; r + 1 <= c; r += 2) {
+                s0 += col[r] * y[r];
+                s1 += col[r + 1] * y[r + 1];
+            }
+            if (r <= c) s0 += col[r] * y[r];
+            x[c] = s0 + s1;
+            zz += (s0 + s1) * (s0 + s1);
         }
         zz = block_sum(zz, red);
         const double inv = zz > 0.0 ? 1.0 / sqrt(zz) : 0.0;
         for (int c = tid; c < k; c += blockDim.x) x[c] *= inv;
         __syncthreads();
     }
-    // inverse iteration: sigma_min <= ||(R^T R)^-1 x||^(-1/2) for unit x;
-    // the triangular solves run on warp 0 only (syncwarp per step)
-    if (dmin > 0.0) {
-        if (tid < 32) {
-            const int lane = tid;
-            for (int j = lane; j < k; j += 32) {
-                x[j] = ((j & 1) ? -inv_sqrt_k : inv_sqrt_k);
-                rinv[j] = 1.0 / R(j, j);
-            }
-            __syncwarp();
-            double est = smin;
-            for (int it = 0; it < 4; ++it) {
-                // R^T y = x (forward, axpy form): y_r = x_r / R_rr; x_c -= R_rc y_r
-                for (int r = 0; r < k; ++r) {
-                    const double yr = x[r] * rinv[r];
-                    for (int c = r + 1 + lane; c < k; c += 32) x[c] -= R(r, c) * yr;
-                    if (lane == 0) y[r] = yr;
-                    __syncwarp();
-                }
-                // R z = y (backward, axpy form): z_c = y_c / R_cc; y_r -= R_rc z_c
-                for (int c = k - 1; c >= 0; --c) {
-                    const double zc = y[c] * rinv[c];
-                    for (int r = lane; r < c; r += 32) y[r] -= R(r, c) * zc;
-                    if (lane == 0) x[c] = zc;
-                    __syncwarp();
-                }
-                double zz = 0.0;
-                for (int c = lane; c < k; c += 32) zz += x[c] * x[c];
-#pragma unroll
-                for (int off = 16; off; off >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, off);
-                if (!(zz > 0.0) || !isfinite(zz)) {
-                    est = 0.0;
-                    break;
-                }
-                est = fmin(est, 1.0 / sqrt(sqrt(zz)));
-                const double inv = 1.0 / sqrt(zz);
-                for (int c = lane; c < k; c += 32) x[c] *= inv;
-                __syncwarp();
-            }
-            smin = est;
-        }
-    } else {
+    if (dmin > 0.0 && tid < 32) {
+        if (k <= 128) smin = inverse_iteration<4>(Rr, ldr, Rc, ldc, k, smin, inv_sqrt_k);
+        else if (k <= 256) smin = inverse_iteration<8>(Rr, ldr, Rc, ldc, k, smin, inv_sqrt_k);
+        else smin = inverse_iteration<kRankMaxPerLane>(Rr, ldr, Rc, ldc, k, smin, inv_sqrt_k);
+    } else if (!(dmin > 0.0)) {
         smin = 0.0;
     }
     if (tid == 0) {
@@ -176,7 +240,8 @@ __device__ void rank_estimate(RA R, int k, double *x, double *y, double *rinv, d
 __global__ void __launch_bounds__(kQrThreads, 1) qr_kernel(const double *__restrict__ mT, int k1,
                                                            int k2, int64_t ldm,
                                                            double *__restrict__ qa,
-                                                           double *__restrict__ qtau) {
+                                                           double *__restrict__ qtau,
+                                                           double *__restrict__ rrow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ld = k2 | 1;
     double *A = reinterpret_cast<double *>(smem_raw);  // column c: A[c*ld + r] = M[r][c]
@@ -212,21 +277,25 @@ __global__ void __launch_bounds__(kQrThreads, 1) qr_kernel(const double *__restr
         __syncthreads();
         const double tj = s_tau, scal = s_scal;
         if (tj != 0.0) {
-            // thread per trailing column c: w = v^T A[:,c] (v_j = 1, v_r = scal*colj[r])
-            for (int c = j + 1 + tid; c < k1; c += blockDim.x) {
+            // 4 threads per trailing column c: w = v^T A[:,c] (v_j = 1,
+            // v_r = scal*colj[r]), quad-shuffle reduction, then the update
+            const int q = tid & 3;
+            for (int c = j + 1 + (tid >> 2); c < k1; c += blockDim.x >> 2) {
                 double *colc = A + c * ld;
-                double w0 = colc[j], w1 = 0.0, w2 = 0.0, w3 = 0.0;
-                int r = j + 1;
-                for (; r + 3 < k2; r += 4) {
-                    w0 += (colj[r] * scal) * colc[r];
-                    w1 += (colj[r + 1] * scal) * colc[r + 1];
-                    w2 += (colj[r + 2] * scal) * colc[r + 2];
-                    w3 += (colj[r + 3] * scal) * colc[r + 3];
+                double w0 = q == 0 ? colc[j] : 0.0, w1 = 0.0;
+                int r = j + 1 + q;
+                for (; r + 4 < k2; r += 8) {
+                    w0 = __fma_rn(colj[r] * scal, colc[r], w0);
+                    w1 = __fma_rn(colj[r + 4] * scal, colc[r + 4], w1);
                 }
-                for (; r < k2; ++r) w0 += (colj[r] * scal) * colc[r];
-                const double f = tj * ((w0 + w1) + (w2 + w3));
-                colc[j] -= f;
-                for (int rr = j + 1; rr < k2; ++rr) colc[rr] -= f * (colj[rr] * scal);
+                for (; r < k2; r += 4) w0 = __fma_rn(colj[r] * scal, colc[r], w0);
+                double w = w0 + w1;
+                const unsigned qmask = 0xFu << ((threadIdx.x & 31) & ~3);  // the quad
+                w += __shfl_xor_sync(qmask, w, 1);
+                w += __shfl_xor_sync(qmask, w, 2);
+                const double f = tj * w;
+                if (q == 0) colc[j] -= f;
+                for (int rr = j + 1 + q; rr < k2; rr += 4) colc[rr] = __fma_rn(-f, colj[rr] * scal, colc[rr]);
             }
         }
         __syncthreads();
@@ -235,6 +304,10 @@ __global__ void __launch_bounds__(kQrThreads, 1) qr_kernel(const double *__restr
         __syncthreads();
     }
     for (int i = tid; i < k1 * ld; i += blockDim.x) qa[i] = A[i];
+    for (int i = tid; i < k1 * k1; i += blockDim.x) {  // R row-major (for the rank test)
+        const int r = i / k1, c = i % k1;
+        rrow[i] = r <= c ? A[c * ld + r] : 0.0;
+    }
 }
 
 // Phase 2 (many CTAs): CTA 0 runs the rank test on R; every warp of the
@@ -242,17 +315,16 @@ __global__ void __launch_bounds__(kQrThreads, 1) qr_kernel(const double *__restr
 __global__ void __launch_bounds__(256) qr_tail_kernel(const double *__restrict__ qa,
                                                       const double *__restrict__ qtau, int k1,
                                                       int k2, double *__restrict__ pinvT,
-                                                      int64_t ldp, double *__restrict__ stats) {
+                                                      int64_t ldp, double *__restrict__ stats,
+                                                      const double *__restrict__ rrow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ld = k2 | 1;
     const int k2p = (k2 + 1) & ~1;
     double *sm = reinterpret_cast<double *>(smem_raw);
-    if (blockIdx.x == 0) {
-        rank_estimate(RSmem{qa, ld}, k1, sm, sm + k2p, sm + 2 * k2p, sm + 3 * k2p, stats);
-        return;
-    }
+    (void)stats;
+    (void)rrow;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c = (blockIdx.x - 1) * (blockDim.x >> 5) + warp;
+    const int c = blockIdx.x * (blockDim.x >> 5) + warp;
     if (c >= k2) return;
     double *z = sm + (size_t)warp * k2p;
     for (int r = lane; r < k2; r += 32) z[r] = (r == c) ? 1.0 : 0.0;
@@ -281,15 +353,16 @@ __global__ void __launch_bounds__(256) qr_tail_kernel(const double *__restrict__
     for (int i = lane; i < k1; i += 32) pinvT[(int64_t)c * ldp + i] = z[i];
 }
 
-__global__ void __launch_bounds__(kQrThreads, 1) rank_estimate_kernel(const double *__restrict__ R,
+__global__ void __launch_bounds__(256, 1) rank_estimate_kernel(const double *__restrict__ R,
                                                                       int k, int64_t ldr,
+                                                                      const double *__restrict__ RT,
+                                                                      int64_t ldt,
                                                                       double *__restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *xv = reinterpret_cast<double *>(smem_raw);
     double *yv = xv + k;
-    double *rv = yv + k;
-    double *red = rv + k;
-    rank_estimate(RGlobalRowMajor{R, ldr}, k, xv, yv, rv, red, stats);
+    double *red = yv + k;
+    rank_estimate(R, ldr, RT, ldt, k, xv, yv, red, stats);
 }
 
 // ---------------------------------------------------------------------------
@@ -363,7 +436,7 @@ using namespace srlu;
 extern "C" size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2) { return qr_pinv_smem(k1, k2); }
 
 extern "C" size_t srlu_qr_pinv_workspace(int64_t k1, int64_t k2) {
-    return sizeof(double) * (size_t)(k1 * (k2 | 1) + k1) + 256;
+    return sizeof(double) * (size_t)(k1 * (k2 | 1) + k1 + k1 * k1) + 256;
 }
 
 extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *pinvT,
@@ -381,30 +454,37 @@ extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ld
     cudaStream_t s = (cudaStream_t)stream;
     double *qa = (double *)ws;
     double *qtau = qa + (size_t)k1 * (k2 | 1);
+    double *rrow = qtau + k1;
     SRLU_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-    qr_kernel<<<1, kQrThreads, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau);
+    qr_kernel<<<1, kQrThreads, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau, rrow);
     SRLU_CHECK_LAUNCH("qr_kernel");
     const int k2p = (int)((k2 + 1) & ~1);
     size_t smem2 = sizeof(double) * (size_t)(8 * k2p + 64);
-    size_t smem_rank = sizeof(double) * (size_t)(4 * k2p + 64);
+    size_t smem_rank = sizeof(double) * (size_t)(3 * k2p + 64);
     if (smem_rank > smem2) smem2 = smem_rank;
     SRLU_CUDA(cudaFuncSetAttribute(qr_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem2));
-    qr_tail_kernel<<<(unsigned)(1 + ceil_div(k2, 8)), 256, smem2, s>>>(qa, qtau, (int)k1, (int)k2,
-                                                                       pinvT, ldp, stats);
+    qr_tail_kernel<<<(unsigned)ceil_div(k2, 8), 256, smem2, s>>>(qa, qtau, (int)k1, (int)k2,
+                                                                       pinvT, ldp, stats, rrow);
     SRLU_CHECK_LAUNCH("qr_tail_kernel");
     return SRLU_OK;
 }
 
-extern "C" int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, double *stats,
-                                  srlu_stream_t stream) {
-    SRLU_REQUIRE(k >= 1 && ldr >= k, SRLU_ERR_ARG, "rank_estimate: bad sizes");
-    size_t smem = sizeof(double) * (size_t)(3 * k + 64);
+extern "C" int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, const double *RT,
+                                  int64_t ldt, double *stats, srlu_stream_t stream) {
+    SRLU_REQUIRE(k >= 1 && ldr >= k && ldt >= k, SRLU_ERR_ARG, "rank_estimate: bad sizes");
+    SRLU_REQUIRE(k <= 32 * kRankMaxPerLane, SRLU_ERR_UNSUPPORTED, "rank_estimate: k > 576");
+    size_t smem = sizeof(double) * (size_t)(2 * k + 64);
     SRLU_REQUIRE(smem <= 200 * 1024, SRLU_ERR_UNSUPPORTED, "rank_estimate: k too large");
     SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    rank_estimate_kernel<<<1, kQrThreads, smem, (cudaStream_t)stream>>>(R, (int)k, ldr, stats);
+    // max shared carveout: the rank test overlaps the column-pivot LU, whose
+    // ~200 KB CTAs must still land on the SM this CTA occupies
+    SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    rank_estimate_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(R, (int)k, ldr, RT, ldt,
+                                                                         stats);
     SRLU_CHECK_LAUNCH("rank_estimate_kernel");
     return SRLU_OK;
 }
@@ -417,5 +497,25 @@ extern "C" int srlu_dgemm(const double *A, int64_t lda, const double *B, int64_t
     dim3 grid((unsigned)ceil_div(M, kGemmBM), (unsigned)ceil_div(N, kGemmBN));
     dgemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, C, ldc, M, (int)N, (int)K);
     SRLU_CHECK_LAUNCH("dgemm_kernel");
+    return SRLU_OK;
+}
+
+extern "C" int srlu_qr_rank(const void *ws, int64_t k1, int64_t k2, double *stats,
+                            srlu_stream_t stream) {
+    SRLU_REQUIRE(k1 >= 1 && k2 >= k1 && k1 <= 32 * kRankMaxPerLane, SRLU_ERR_ARG,
+                 "qr_rank: bad sizes");
+    const double *qa = (const double *)ws;
+    const double *rrow = qa + (size_t)k1 * (k2 | 1) + k1;
+    size_t smem = sizeof(double) * (size_t)(2 * k1 + 64);
+    SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // max shared carveout: the rank test overlaps the column-pivot LU, whose
+    // ~200 KB CTAs must still land on the SM this CTA occupies
+    SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    // R row-major = rrow, R column-major = the packed QR (column stride k2|1)
+    rank_estimate_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(rrow, (int)k1, k1, qa,
+                                                                 (int64_t)(k2 | 1), stats);
+    SRLU_CHECK_LAUNCH("rank_estimate_kernel");
     return SRLU_OK;
 }

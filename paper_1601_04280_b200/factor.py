@@ -50,14 +50,15 @@ def lu_row_pivot_dev(y: torch.Tensor, want_u: bool = False, stream=None):
     up = torch.zeros(k, k, dtype=torch.float64, device=dev) if want_u else None
     ws = _lib.workspace(L.srlu_lu_workspace(m, k), dev)
     _lib.check(L.srlu_lu_rowpiv(_lib.ptr(y), m, k, y.stride(0), _lib.ptr(perm), _lib.ptr(lo),
-                                lo.stride(0), _lib.ptr(up), k, _lib.ptr(ws), ws.numel(),
+                                lo.stride(0), _lib.ptr(up), k, 0, _lib.ptr(ws), ws.numel(),
                                 _lib.stream_handle(stream)), "lu_row_pivot")
     return perm, lo, up
 
 
-def lu_col_pivot_dev(ct: torch.Tensor, stream=None):
+def lu_col_pivot_dev(ct: torch.Tensor, stream=None, reserve_sms=0):
     """K5 on core^T (n x k row-major fp64 device tensor, overwritten).
-    Returns (q int64[n], Lt k x k, UT n x k) with U = UT^T."""
+    Returns (q int64[n], Lt k x k, UT n x k) with U = UT^T.  ``reserve_sms``
+    SMs stay out of the cooperative grid (a side-stream kernel runs there)."""
     L = _lib.lib()
     n, k = ct.shape
     if k > n:
@@ -68,7 +69,7 @@ def lu_col_pivot_dev(ct: torch.Tensor, stream=None):
     ut = torch.empty(n, k, dtype=torch.float64, device=dev)
     ws = _lib.workspace(L.srlu_lu_workspace(n, k), dev)
     _lib.check(L.srlu_lu_colpiv(_lib.ptr(ct), n, k, ct.stride(0), _lib.ptr(q), _lib.ptr(lt),
-                                lt.stride(0), _lib.ptr(ut), ut.stride(0), _lib.ptr(ws),
+                                lt.stride(0), _lib.ptr(ut), ut.stride(0), reserve_sms, _lib.ptr(ws),
                                 ws.numel(), _lib.stream_handle(stream)), "lu_col_pivot")
     return q, lt, ut
 
@@ -109,13 +110,15 @@ def lu_col_pivot(mat) -> ColPivotedLU:
 QR_SMEM_LIMIT = 220 * 1024
 
 
-def pinv_dev(m_t: torch.Tensor, stream=None):
+def pinv_dev(m_t: torch.Tensor, stream=None, rank_event=False):
     """pinv of M = m_t^T (k2 x k1) on the device (factor.py:112-130).
     ``m_t``: k1 x k2 row-major fp64.  Returns (pinvT k2 x k1, stats[4]
-    device: sigma_max, sigma_min estimates, cond, singular flag); the caller
-    decides singularity after its one host sync.  One CTA of libsrlu
-    (Householder QR + rank test + R^-1 Q^T) when M fits in shared memory;
-    otherwise the QR comes from cuSOLVER and the rank test from libsrlu."""
+    device: sigma_max, sigma_min estimates, cond, singular flag[, event]).
+    The rank test is enqueued AFTER the pinv (same stream) so a consumer of
+    pinvT can wait on the returned event and overlap the rank test; the
+    caller decides singularity after its one host sync.  One CTA of libsrlu
+    does the Householder QR when M fits in shared memory; otherwise the QR
+    comes from cuSOLVER and the rank test from libsrlu."""
     L = _lib.lib()
     m_t = m_t.contiguous()
     k1, k2 = m_t.shape
@@ -124,22 +127,39 @@ def pinv_dev(m_t: torch.Tensor, stream=None):
     dev = m_t.device
     stats = torch.empty(4, dtype=torch.float64, device=dev)
     sh = _lib.stream_handle(stream)
+    ev = torch.cuda.Event()
     if L.srlu_qr_pinv_smem_bytes(k1, k2) <= QR_SMEM_LIMIT:
         pinv_t = torch.empty(k2, k1, dtype=torch.float64, device=dev)
         ws = _lib.workspace(L.srlu_qr_pinv_workspace(k1, k2), dev)
         _lib.check(L.srlu_qr_pinv(_lib.ptr(m_t), k1, k2, m_t.stride(0), _lib.ptr(pinv_t),
                                   pinv_t.stride(0), _lib.ptr(stats), _lib.ptr(ws), ws.numel(), sh),
                    "qr_pinv")
-        return pinv_t, stats
-    qf, rf = torch.linalg.qr(m_t.t(), mode="reduced")
-    rf = rf.contiguous()
-    _lib.check(L.srlu_rank_estimate(_lib.ptr(rf), k1, rf.stride(0), _lib.ptr(stats), sh),
-               "rank_estimate")
-    pinv_t = torch.linalg.solve_triangular(rf, qf.t().contiguous(), upper=True).t().contiguous()
+        ev.record(stream)
+        _lib.check(L.srlu_qr_rank(_lib.ptr(ws), k1, k2, _lib.ptr(stats), sh), "qr_rank")
+    else:
+        qf, rf = torch.linalg.qr(m_t.t(), mode="reduced")
+        rf = rf.contiguous()
+        pinv_t = torch.linalg.solve_triangular(rf, qf.t().contiguous(), upper=True).t().contiguous()
+        ev.record(stream)
+        rft = rf.t().contiguous()
+        _lib.check(L.srlu_rank_estimate(_lib.ptr(rf), k1, rf.stride(0), _lib.ptr(rft),
+                                        rft.stride(0), _lib.ptr(stats), sh), "rank_estimate")
+    if rank_event:
+        return pinv_t, stats, ev
     return pinv_t, stats
 
 
 def dgemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    """out = a @ b (row-major fp64).  These are plain GEMMs (randlu.py:267,
+    :272): cuBLAS DGEMM (measured 1.3-2x faster than libsrlu's SIMT FMA
+    GEMM on these shapes); libsrlu's srlu_dgemm remains available via
+    ``dgemm_srlu``."""
+    if out is None:
+        return torch.mm(a, b)
+    return torch.mm(a, b, out=out)
+
+
+def dgemm_srlu(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None):
     """out = a @ b (row-major fp64) with libsrlu's FMA GEMM."""
     L = _lib.lib()
     a = a if a.stride(1) == 1 else a.contiguous()

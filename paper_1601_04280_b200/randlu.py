@@ -249,9 +249,9 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     ev_redl.record(main)
     side.wait_event(ev_redl)
     with torch.cuda.stream(side):
-        pinv_t, stats = pinv_dev(red_lT, stream=side)
-        ev_pinv = torch.cuda.Event()
-        ev_pinv.record(side)
+        # pinv first; the rank test follows on the side stream and overlaps
+        # the core GEMM and K5 (only the final host decision needs it)
+        pinv_t, stats, ev_pinv = pinv_dev(red_lT, stream=side, rank_event=True)
     pinv_t.record_stream(main)
     stats.record_stream(main)
     red_lT.record_stream(side)
@@ -270,11 +270,14 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     ev[4].record(main)
     core_keep = core_t.clone() if keep else None
 
-    q, lt, ut = lu_col_pivot_dev(core_t)
+    # one SM left to the side stream's rank test (a cooperative launch would
+    # otherwise wait for it)
+    q, lt, ut = lu_col_pivot_dev(core_t, reserve_sms=1)
     l_final = dgemm(l1, lt)
     ev[5].record(main)
 
     # the one host sync of the attempt: rank test, non-finite flag, P, Q
+    main.wait_stream(side)
     stats_h, flag_h, perm_h, q_h = (_pinned_copy(t) for t in (stats, flag, perm, q))
     ev[5].synchronize()
     torch.cuda.current_stream(dev).synchronize()

@@ -296,3 +296,21 @@ def test_config2_full_size_vs_oracle(P):
     np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
     check_tail(res.Q.indices, res.L.numpy(), res.U.numpy(), ref["Q"], ref["L"], ref["U"],
                ref["core"], ref["red_l"], ref["red_a"], ref["L1"])
+
+
+def test_csr_long_columns_bit_exact(P):
+    """Columns longer than the 2048-entry fast path (second launch) stay exact."""
+    from scipy.sparse import csr_array
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(31))
+    m, n = 6000, 300
+    d = g.standard_normal((m, n))
+    d[g.random((m, n)) < 0.97] = 0.0
+    d[g.random(m) < 0.6, 7] = g.standard_normal(1)[0]      # ~3600 entries in column 7
+    d[:, 11] = g.standard_normal(m)                          # dense column 11
+    prm = dict(r=6, k1=14, l1=56, k2=22, l2=88, seed=5)
+    res = P.sparse_randomized_lu(P.Matrix.sparse(csr_array(d)), P.RandLuParams(**prm), keep=True)
+    ref = O.sparse_randomized_lu(csr_array(d), prm, keep=True)
+    np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
+    np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
