@@ -21,9 +21,33 @@
 //     with the pivot entities' trailing vectors obtained by the small
 //     in-panel triangular recurrence.
 // Result: P/Q and L/U bit-identical to the reference on the same input.
+#include <cooperative_groups.h>
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "tma.cuh"
+
+namespace cg = cooperative_groups;
+
+#ifdef SRLU_LU_TRACE
+__device__ long long g_lu_trace[8];
+#define LU_T0() long long t_prev_ = clock64(), t_acc_[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define LU_T(i)                                                  \
+    do {                                                         \
+        long long t_ = clock64();                                \
+        t_acc_[i] += t_ - t_prev_;                               \
+        t_prev_ = t_;                                            \
+    } while (0)
+#define LU_TDUMP()                                                            \
+    do {                                                                      \
+        if (threadIdx.x == 0 && blockIdx.x == 0)                              \
+            for (int i_ = 0; i_ < 8; ++i_) g_lu_trace[i_] = t_acc_[i_];       \
+    } while (0)
+#else
+#define LU_T0() do { } while (0)
+#define LU_T(i) do { } while (0)
+#define LU_TDUMP() do { } while (0)
+#endif
 
 namespace srlu {
 
@@ -331,6 +355,439 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     for (int e = tid; e < ne; e += blockDim.x) p.perm[pos[e]] = e0 + e;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster variant: the same replay (identical per-element operation order,
+// so identical results) on ONE thread-block cluster of CL CTAs (16 when the
+// device allows non-portable clusters) x 1024 threads, one entity per
+// thread, for matrices whose panels fit the cluster's shared memory
+// (BASELINE configs 1-2: Y and core stay L2-resident).
+//  * attribute-major working copy: the kernel first transposes its entities
+//    into wt[x][e] (workspace), so every per-entity access of the panel loads,
+//    write-backs and trailing updates is a coalesced warp access;
+//  * exchange without a cluster-wide barrier: after the CTA argmax, warp d
+//    (d < CL) writes {candidate, the candidate's panel row} into slot
+//    [s&1][rank] of CTA d's shared memory with st.async, whose bytes complete
+//    the transaction count of CTA d's mbarrier for that slot; each CTA waits
+//    on its own mbarrier (armed with the step's byte count) and every warp
+//    reduces the CL candidates locally.  Slots are double-buffered: a
+//    producer can write slot s&1 again only at step s+2, after it received
+//    every CTA's step-(s+1) push, which each CTA sends only after all its
+//    threads finished step s (the argmax barriers in between);
+//  * deferred trailing update: the panel's pivot entities' trailing values are
+//    staged in shared memory once, the small triangular recurrence runs there,
+//    and each thread updates its entity in blocks of 8 independent columns.
+__device__ __forceinline__ unsigned mapa_rank(unsigned saddr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f64x2(unsigned addr, double a, double b) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u64x2(unsigned addr, unsigned long long a,
+                                                 unsigned long long b) {
+    asm volatile("st.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void st_async_f64x2(unsigned addr, double a, double b, unsigned rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+        "d"(a), "d"(b), "r"(rbar)
+        : "memory");
+}
+__device__ __forceinline__ void st_async_u64x2(unsigned addr, unsigned long long a,
+                                               unsigned long long b, unsigned rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+        "l"(a), "l"(b), "r"(rbar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cta(unsigned addr, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(addr),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init_cta(unsigned addr, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned raddr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned addr, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+struct LuClusterParams {
+    LuParams p;
+    double *wt;   // k x ldt attribute-major working copy
+    int64_t ldt;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ unsigned long long s_wabs[2][32];
+    __shared__ unsigned s_wkey[2][32];
+    __shared__ unsigned long long s_babs[2];
+    __shared__ unsigned s_bkey[2];
+    __shared__ double s_wsum[32];
+    __shared__ double s_thresh;
+    __shared__ __align__(8) uint64_t xbar[2];
+
+    const LuParams &p = cp.p;
+    double *const wt = cp.wt;
+    const int64_t ldt = cp.ldt;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int CL = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int k = p.k, b = p.b, bs = p.bs, rpc = p.rpc;
+    const int b2 = (b + 1) & ~1;       // slot row length (16-byte rows)
+    const int AW = ((k > b ? k - b : 1) + 15) & ~15;  // widest trailing block, 16-padded
+    const int64_t e0 = (int64_t)rank * rpc;
+    const int ne = (int)max((int64_t)0, min((int64_t)rpc, p.M - e0));
+    const bool mine = tid < ne;  // thread tid owns entity e0 + tid
+    const int64_t me = e0 + tid;
+
+    double *xrow = reinterpret_cast<double *>(smem_raw);     // [2][CL][b2]
+    Cand *xcand = reinterpret_cast<Cand *>(xrow + (size_t)2 * CL * b2);  // [2][CL]
+    double *xpart = reinterpret_cast<double *>(xcand + 2 * CL);          // [CL]
+    double *ucol = xpart + CL;                                           // [32][b]
+    double *PR = ucol + 32 * b;                                          // b x b
+    double *Ach = PR + (((size_t)b * b + 1) & ~(size_t)1);               // b x AW (16-B aligned)
+    double *panel = Ach + (size_t)b * AW;                                // rpc x bs
+    int *pw_ent = reinterpret_cast<int *>(panel + (size_t)rpc * bs);     // b
+    int *qarr = pw_ent + b;                                              // rpc (epilogue)
+    // transposes go through tiles of TWD columns in the panel region
+    const int TWD = max(1, min(16, bs - 1));
+    double *myrow = panel + (size_t)tid * bs;
+    int mypos = (int)me;
+
+    // CTA argmax of (|w| desc, position asc); key = pos << 10 | local entity
+    auto cta_argmax = [&](unsigned long long a, unsigned key, int par) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const unsigned long long oa = __shfl_xor_sync(0xffffffffu, a, off);
+            const unsigned ok = __shfl_xor_sync(0xffffffffu, key, off);
+            if (better(oa, ok, a, key)) { a = oa; key = ok; }
+        }
+        if (lane == 0) { s_wabs[par][warp] = a; s_wkey[par][warp] = key; }
+        __syncthreads();
+        if (warp == 0) {
+            a = lane < nwarps ? s_wabs[par][lane] : 0ULL;
+            key = lane < nwarps ? s_wkey[par][lane] : 0xFFFFFFFFu;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long oa = __shfl_xor_sync(0xffffffffu, a, off);
+                const unsigned ok = __shfl_xor_sync(0xffffffffu, key, off);
+                if (better(oa, ok, a, key)) { a = oa; key = ok; }
+            }
+            if (lane == 0) { s_babs[par] = a; s_bkey[par] = key; }
+        }
+        __syncthreads();
+    };
+
+    // bytes every CTA receives for step s: CL x {row pairs, candidate}
+    auto step_bytes = [&](int st) -> unsigned {
+        const int bw_s = min(b, k - (st / b) * b);
+        return (unsigned)(CL * (((bw_s + 1) >> 1) * 16 + 16));
+    };
+    if (tid == 0) {
+        mbar_init_cta(smem_u32(&xbar[0]), 1u);
+        mbar_init_cta(smem_u32(&xbar[1]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_arrive_expect_tx_cta(smem_u32(&xbar[0]), step_bytes(0));
+        if (k > 1) mbar_arrive_expect_tx_cta(smem_u32(&xbar[1]), step_bytes(1));
+    }
+    // ---- transpose own entities into wt (through shared-memory tiles, full
+    // 128-byte rows read by 16 consecutive threads); ||w||_F^2 on the way ----
+    double ss = 0.0;
+    for (int x0 = 0; x0 < k; x0 += TWD) {
+        const int cw = min(TWD, k - x0);
+        for (int t = tid; t < ne * 16; t += blockDim.x) {
+            const int e = t >> 4, c = t & 15;
+            if (c < cw) panel[(size_t)e * bs + c] = p.w[(e0 + e) * p.ld + x0 + c];
+        }
+        __syncthreads();
+        if (mine)
+            for (int c = 0; c < cw; ++c) {
+                const double v = myrow[c];
+                wt[(int64_t)(x0 + c) * ldt + me] = v;
+                ss += v * v;
+            }
+        __syncthreads();
+    }
+    cl.sync();  // barriers initialised, every CTA running, before any remote access
+    {  // thresh = PIVOT_RTOL * ||w||_F (fixed-order two-level sum)
+#pragma unroll
+        for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        if (lane == 0) s_wsum[warp] = ss;
+        __syncthreads();
+        if (warp == 0) {
+            double v = lane < nwarps ? s_wsum[lane] : 0.0;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane < CL) *cl.map_shared_rank(xpart + rank, lane) = v;
+        }
+        cl.sync();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int c = 0; c < CL; ++c) tot += xpart[c];
+            s_thresh = kPivotRtol * sqrt(tot);
+        }
+        __syncthreads();
+    }
+    const double thresh = s_thresh;
+    LU_T0();
+
+    for (int J = 0; J < k; J += b) {
+        const int bw = min(b, k - J);
+        if (mine)
+            for (int x = 0; x < bw; ++x) myrow[x] = wt[(int64_t)(J + x) * ldt + me];
+        {  // candidates for the panel's first column
+            unsigned long long a = 0ULL;
+            unsigned key = 0xFFFFFFFFu;
+            if (mine && mypos >= J) {
+                a = (unsigned long long)__double_as_longlong(fabs(myrow[0]));
+                key = ((unsigned)mypos << 10) | (unsigned)tid;
+            }
+            cta_argmax(a, key, J & 1);
+        }
+        LU_T(6);
+
+        for (int ls = 0; ls < bw; ++ls) {
+            const int s = J + ls;
+            const int slot = s & 1;
+            // 1. warp d pushes {candidate, its panel row} into CTA d's slot
+            if (warp < CL) {
+                const unsigned long long babs = s_babs[slot];
+                const unsigned bkey = s_bkey[slot];
+                const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);
+                const unsigned dst = (unsigned)warp;
+                const int npair = (bw + 1) >> 1;
+                if (lane < npair) {
+                    const int x = 2 * lane;
+                    double v0 = 0.0, v1 = 0.0;
+                    if (owner >= 0) {
+                        v0 = panel[(size_t)owner * bs + x];
+                        v1 = x + 1 < bw ? panel[(size_t)owner * bs + x + 1] : 0.0;
+                    }
+                    st_async_f64x2(
+                        mapa_rank(smem_u32(xrow + ((size_t)slot * CL + rank) * b2 + x), dst), v0, v1,
+                        mapa_rank(smem_u32(&xbar[slot]), dst));
+                } else if (lane == 31) {
+                    const unsigned pos = owner >= 0 ? (bkey >> 10) : 0xFFFFFFFFu;
+                    const int ent = owner >= 0 ? (int)(e0 + owner) : -1;
+                    st_async_u64x2(mapa_rank(smem_u32(xcand + slot * CL + rank), dst), babs,
+                                   ((unsigned long long)(unsigned)ent << 32) | pos,
+                                   mapa_rank(smem_u32(&xbar[slot]), dst));
+                }
+            }
+            LU_T(1);
+            // 2. wait for the CL pushes of this step
+            mbar_wait_cluster(smem_u32(&xbar[slot]), (unsigned)((s >> 1) & 1));
+            // re-arm this slot for step s+2 (its data can only arrive after
+            // this CTA's own step-(s+1) push, which follows in program order)
+            if (tid == 0 && s + 2 < k) mbar_arrive_expect_tx_cta(smem_u32(&xbar[slot]), step_bytes(s + 2));
+            LU_T(2);
+            // 3. winner: every warp reduces the CL candidates itself
+            unsigned long long ga = 0ULL;
+            unsigned gkey = 0xFFFFFFFFu;
+            if (lane < CL) {
+                const Cand c = xcand[slot * CL + lane];
+                if (c.entity >= 0) { ga = c.absbits; gkey = (c.pos << 4) | (unsigned)lane; }
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ga, off);
+                const unsigned ok = __shfl_xor_sync(0xffffffffu, gkey, off);
+                if (better(oa, ok, ga, gkey)) { ga = oa; gkey = ok; }
+            }
+            const int gc = (int)(gkey & 15u);
+            const int wpos = (int)(gkey >> 4);
+            const int went = xcand[slot * CL + gc].entity;
+            const double *u = xrow + ((size_t)slot * CL + gc) * b2;
+            const double pivv = u[ls];
+            const bool big = fabs(pivv) > thresh;
+            if (tid == 0) pw_ent[ls] = went;
+            if (b < k && tid < bw)
+                PR[ls * b + tid] = (MODE == MODE_COL && tid > ls) ? (big ? u[tid] / pivv : 0.0)
+                                                                  : u[tid];
+            // 4. swap positions s <-> wpos (own entity only)
+            if (mine) {
+                if (mypos == s) mypos = wpos;
+                if (me == went) mypos = s;
+            }
+            const double *um = u;
+            if (MODE == MODE_COL) {  // this warp's copy of the multipliers
+                double *uw = ucol + warp * b;
+                if (lane > ls && lane < bw) uw[lane] = big ? u[lane] / pivv : 0.0;
+                __syncwarp();
+                um = uw;
+            }
+            LU_T(3);
+            // 5. update own panel row (next pivot column first)
+            if (mine) {
+                if (MODE == MODE_ROW) {
+                    if (mypos > s) {
+                        if (big) {
+                            const double lm = myrow[ls] / pivv;
+                            myrow[ls] = lm;
+                            for (int x = ls + 1; x < bw; ++x)
+                                myrow[x] = __dsub_rn(myrow[x], __dmul_rn(lm, u[x]));
+                        } else {
+                            myrow[ls] = 0.0;
+                        }
+                    }
+                } else {
+                    if (me == went) {
+                        for (int x = ls + 1; x < bw; ++x) myrow[x] = um[x];
+                    } else if (mypos > s && big) {
+                        const double lm = myrow[ls];
+                        for (int x = ls + 1; x < bw; ++x)
+                            myrow[x] = __dsub_rn(myrow[x], __dmul_rn(um[x], lm));
+                    }
+                }
+            }
+            LU_T(4);
+            if (ls + 1 < bw) {
+                unsigned long long a = 0ULL;
+                unsigned key = 0xFFFFFFFFu;
+                if (mine && mypos >= s + 1) {
+                    a = (unsigned long long)__double_as_longlong(fabs(myrow[ls + 1]));
+                    key = ((unsigned)mypos << 10) | (unsigned)tid;
+                }
+                cta_argmax(a, key, (s + 1) & 1);
+            }
+            LU_T(0);
+        }
+        __syncthreads();  // PR / pw_ent complete
+
+        // write the panel back
+        if (mine)
+            for (int x = 0; x < bw; ++x) wt[(int64_t)(J + x) * ldt + me] = myrow[x];
+
+        // deferred trailing update of columns [J+bw, k)
+        const int x0 = J + bw, tw = k - x0;
+        if (tw > 0) {
+            const int twp = (tw + 15) & ~15;
+            for (int t = tid; t < bw * twp; t += blockDim.x) {
+                const int ls = t / twp, c = t % twp;
+                Ach[ls * AW + c] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + pw_ent[ls]) : 0.0;
+            }
+            __syncthreads();
+            for (int c = tid; c < tw; c += blockDim.x) {
+                for (int ls = 0; ls < bw; ++ls) {
+                    double v = Ach[ls * AW + c];
+                    const double *pr = PR + ls * b;
+                    if (MODE == MODE_ROW) {
+                        for (int l2 = 0; l2 < ls; ++l2)
+                            v = __dsub_rn(v, __dmul_rn(pr[l2], Ach[l2 * AW + c]));
+                    } else {
+                        for (int l2 = 0; l2 < ls; ++l2)
+                            v = __dsub_rn(v, __dmul_rn(Ach[l2 * AW + c], pr[l2]));
+                        const double pv = pr[ls];
+                        v = fabs(pv) > thresh ? v / pv : 0.0;
+                    }
+                    Ach[ls * AW + c] = v;
+                    if (rank == 0) p.piv[(int64_t)(J + ls) * k + x0 + c] = v;
+                }
+            }
+            __syncthreads();
+            if (mine && mypos >= x0) {  // pivots are frozen
+                double *g = wt + (int64_t)x0 * ldt + me;
+                for (int c0 = 0; c0 < tw; c0 += 16) {
+                    double v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = c0 + i < tw ? g[(int64_t)(c0 + i) * ldt] : 0.0;
+                    for (int ls = 0; ls < bw; ++ls) {
+                        const double l = myrow[ls];
+                        const double2 *ar = reinterpret_cast<const double2 *>(Ach + ls * AW + c0);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const double2 av = ar[i];  // zero-padded past tw
+                            if (MODE == MODE_ROW) {
+                                v[2 * i] = __dsub_rn(v[2 * i], __dmul_rn(l, av.x));
+                                v[2 * i + 1] = __dsub_rn(v[2 * i + 1], __dmul_rn(l, av.y));
+                            } else {
+                                v[2 * i] = __dsub_rn(v[2 * i], __dmul_rn(av.x, l));
+                                v[2 * i + 1] = __dsub_rn(v[2 * i + 1], __dmul_rn(av.y, l));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (c0 + i < tw) g[(int64_t)(c0 + i) * ldt] = v[i];
+                }
+            }
+            __syncthreads();
+        }
+        LU_T(5);
+    }
+    LU_TDUMP();
+
+    // ---- final assembly (after everyone's write-backs and rank 0's piv rows):
+    // each entity's output row goes through a shared-memory tile so that 16
+    // consecutive threads write 128 contiguous bytes of row q
+    cl.sync();
+    if (mine) {
+        qarr[tid] = mypos;
+        p.perm[mypos] = me;
+    }
+    const int q = mypos;
+    const int pend = q < k ? min(k, (q / b) * b + b) : k;
+    for (int x0 = 0; x0 < k; x0 += TWD) {
+        const int cw = min(TWD, k - x0);
+        if (mine)
+            for (int c = 0; c < cw; ++c) {
+                const int x = x0 + c;
+                const double v =
+                    x < pend ? wt[(int64_t)x * ldt + me] : __ldcg(p.piv + (int64_t)q * k + x);
+                double o;
+                if (MODE == MODE_ROW) {
+                    o = q >= k ? v : (x < q ? v : (x == q ? 1.0 : 0.0));
+                    if (q < k && p.out_small) p.out_small[(int64_t)q * p.ld_small + x] = x >= q ? v : 0.0;
+                } else {
+                    o = (q >= k || x <= q) ? v : 0.0;
+                    if (q < k) p.out_small[(int64_t)x * p.ld_small + q] = x > q ? v : (x == q ? 1.0 : 0.0);
+                }
+                myrow[c] = o;
+            }
+        __syncthreads();
+        for (int t = tid; t < ne * 16; t += blockDim.x) {
+            const int e = t >> 4, c = t & 15;
+            if (c < cw) p.out_main[(int64_t)qarr[e] * p.ld_main + x0 + c] = panel[(size_t)e * bs + c];
+        }
+        __syncthreads();
+    }
+    cl.sync();  // no CTA exits while a peer could still address its shared memory
+}
+
+static size_t lu_cluster_smem_bytes(int rpc, int b, int bs, int CL, int k) {
+    const int AW = ((k > b ? k - b : 1) + 15) & ~15;
+    const int b2 = (b + 1) & ~1;
+    return sizeof(double) * ((size_t)2 * CL * b2 + CL + (size_t)32 * b + (((size_t)b * b + 1) & ~(size_t)1) +
+                             (size_t)b * AW + (size_t)rpc * bs) +
+           sizeof(Cand) * 2 * CL + sizeof(int) * ((size_t)b + rpc) + 16;
+}
+
+// the cluster path is considered for M <= 16 * 1024 entities
+constexpr int64_t kLuClusterMaxM = 16 * 1024;
+static inline int64_t lu_cluster_ldt(int64_t M) { return (M + 31) & ~(int64_t)31; }
+static size_t lu_base_workspace(int64_t k) {
+    return 256 + sizeof(double) * kLuMaxGrid + sizeof(Cand) * 2 * kLuMaxGrid +
+           sizeof(double) * ((size_t)2 * kLuMaxGrid * k + (size_t)k * k) + 256;
+}
+
 static size_t lu_smem_bytes(int rpc, int b, int bs) {
     return sizeof(double) * ((size_t)rpc * bs + (size_t)b * b + b + (size_t)b * kLuXC) +
            sizeof(int) * ((size_t)rpc + b) + 16;
@@ -343,6 +800,68 @@ static int sm_count() {
     return n > 0 ? n : 1;
 }
 
+// Cluster path when the panels of all M entities fit one cluster's shared
+// memory with a useful panel width; returns SRLU_OK when launched, 1 when the
+// shape (or the device) does not qualify.
+template <int MODE>
+static int try_run_lu_cluster(LuParams prm, void *ws, cudaStream_t stream) {
+    if (const char *env = getenv("SRLU_LU_NO_CLUSTER"))  // testing knob
+        if (atoi(env)) return 1;
+    const int64_t M = prm.M;
+    const int k = prm.k;
+    if (M > kLuClusterMaxM || k > 1024) return 1;
+    auto kern = lu_cluster_kernel<MODE>;
+    const size_t budget = 220 * 1024;
+    for (int CL : {16, 8}) {
+        const int64_t rpc64 = ceil_div(M, (int64_t)CL);
+        if (rpc64 > 1024) continue;  // one entity per thread
+        const int rpc = (int)rpc64;
+        int b = k < 32 ? k : 32;  // slot rows / per-warp multipliers hold <= 32
+        while (b > 1 && lu_cluster_smem_bytes(rpc, b, b | 1, CL, k) > budget) --b;
+        if (b < (k < 8 ? k : 8) || lu_cluster_smem_bytes(rpc, b, b | 1, CL, k) > budget) continue;
+        const size_t smem = lu_cluster_smem_bytes(rpc, b, b | 1, CL, k);
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return 1;
+        }
+        if (CL > 8 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(CL);
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (void *)kern, &cfg) != cudaSuccess ||
+            nclusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        LuClusterParams cp;
+        cp.p = prm;
+        cp.p.b = b;
+        cp.p.bs = b | 1;
+        cp.p.rpc = rpc;
+        cp.ldt = lu_cluster_ldt(M);
+        cp.wt = (double *)((char *)ws + ((lu_base_workspace(k) + 255) & ~(size_t)255));
+        SRLU_CUDA(cudaLaunchKernelEx(&cfg, kern, cp));
+        return SRLU_OK;
+    }
+    return 1;
+}
+
 template <int MODE>
 static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, double *out_main,
                   int64_t ld_main, double *out_small, int64_t ld_small, int reserve_sms,
@@ -352,6 +871,21 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     SRLU_REQUIRE(M < (1LL << 31) - 1 && k <= 8192, SRLU_ERR_UNSUPPORTED, "lu: sizes too large");
     SRLU_REQUIRE(ws_bytes >= srlu_lu_workspace(M, k), SRLU_ERR_WORKSPACE, "lu: workspace too small");
     SRLU_REQUIRE(reserve_sms >= 0, SRLU_ERR_ARG, "lu: reserve_sms < 0");
+
+    char *wsb = (char *)ws;
+    LuParams prm;
+    prm.w = w; prm.M = M; prm.k = (int)k; prm.ld = ld;
+    prm.perm = perm; prm.out_main = out_main; prm.ld_main = ld_main;
+    prm.out_small = out_small; prm.ld_small = ld_small;
+    prm.bar = (unsigned *)wsb;
+    prm.partial = (double *)(wsb + 256);
+    prm.cand = (Cand *)(wsb + 256 + sizeof(double) * kLuMaxGrid);
+    prm.candrow = (double *)((char *)prm.cand + sizeof(Cand) * 2 * kLuMaxGrid);
+    prm.piv = prm.candrow + (size_t)2 * kLuMaxGrid * k;
+
+    const int rc = try_run_lu_cluster<MODE>(prm, ws, stream);
+    if (rc <= 0) return rc;  // launched (0) or failed (<0)
+
     int G = sm_count() - reserve_sms;
     if (G < 1) G = 1;
     if (const char *env = getenv("SRLU_LU_MAX_GRID")) {  // testing knob
@@ -375,17 +909,7 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     int per_sm = 0;
     SRLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLuThreads, smem));
     SRLU_REQUIRE(per_sm >= 1, SRLU_ERR_UNSUPPORTED, "lu: kernel cannot be resident");
-
-    char *wsb = (char *)ws;
-    LuParams prm;
-    prm.w = w; prm.M = M; prm.k = (int)k; prm.ld = ld; prm.b = b; prm.bs = bs; prm.rpc = rpc;
-    prm.perm = perm; prm.out_main = out_main; prm.ld_main = ld_main;
-    prm.out_small = out_small; prm.ld_small = ld_small;
-    prm.bar = (unsigned *)wsb;
-    prm.partial = (double *)(wsb + 256);
-    prm.cand = (Cand *)(wsb + 256 + sizeof(double) * kLuMaxGrid);
-    prm.candrow = (double *)((char *)prm.cand + sizeof(Cand) * 2 * kLuMaxGrid);
-    prm.piv = prm.candrow + (size_t)2 * kLuMaxGrid * k;
+    prm.b = b; prm.bs = bs; prm.rpc = rpc;
     SRLU_CUDA(cudaMemsetAsync(prm.bar, 0, 256, stream));
     void *args[] = {&prm};
     SRLU_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(kLuThreads), args, smem,
@@ -398,9 +922,10 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
 using namespace srlu;
 
 extern "C" size_t srlu_lu_workspace(int64_t M, int64_t k) {
-    (void)M;
-    return 256 + sizeof(double) * kLuMaxGrid + sizeof(Cand) * 2 * kLuMaxGrid +
-           sizeof(double) * ((size_t)2 * kLuMaxGrid * k + (size_t)k * k) + 256;
+    size_t n = lu_base_workspace(k);
+    if (M <= kLuClusterMaxM && k <= 1024)  // attribute-major copy for the cluster path
+        n = ((n + 255) & ~(size_t)255) + sizeof(double) * (size_t)k * lu_cluster_ldt(M);
+    return n;
 }
 
 extern "C" int srlu_lu_rowpiv(double *y, int64_t m, int64_t k, int64_t ldy, int64_t *perm,

@@ -19,11 +19,18 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "tma.cuh"
+
+#ifdef SRLU_QR_TRACE
+__device__ long long g_qr_trace[256][6];
+#define QR_T(c, i) \
+    do { if ((threadIdx.x % 8) == 0) g_qr_trace[c][i] = clock64(); } while (0)
+#else
+#define QR_T(c, i) do { } while (0)
+#endif
 
 namespace srlu {
 
-constexpr int kQrThreads = 512;
-constexpr int kQrWarps = kQrThreads / 32;
 constexpr double kRankRtol = 1e-10;  // factor.py:22
 
 __device__ inline double block_sum(double v, double *red) {
@@ -75,6 +82,7 @@ __device__ inline double block_min(double v, double *red) {
 //    j == l mod 32) and the next row/column prefetched, so each of the k
 //    sequential steps costs one shuffle broadcast + k/32 FMAs.
 constexpr int kRankMaxPerLane = 18;  // k <= 576
+constexpr int kTailMaxPer = 8;       // register-resident pinv columns: k2 <= 256
 
 // warp 0: 3 inverse iterations, vectors distributed over lane registers
 // (lane l owns entries j == l mod 32, PER per lane), next row prefetched.
@@ -233,96 +241,251 @@ __device__ void rank_estimate(const double *__restrict__ Rr, int64_t ldr,
     }
 }
 
-// Phase 1 (one CTA): Householder QR of M in shared memory; the packed
-// reflectors/R (column-major, stride ld) and tau go to global memory.
-// Reflector j is formed by warp 0 (norm + dlarfg); applying it to the
-// trailing columns is one thread per column (dot + axpy over the column).
-__global__ void __launch_bounds__(kQrThreads, 1) qr_kernel(const double *__restrict__ mT, int k1,
-                                                           int k2, int64_t ldm,
-                                                           double *__restrict__ qa,
-                                                           double *__restrict__ qtau,
-                                                           double *__restrict__ rrow) {
+// Phase 1 (one CTA): Householder QR of M in shared memory (LAPACK dgeqr2 /
+// dlarfg conventions); the packed reflectors/R (column-major, stride ld),
+// tau and R row-major (for the rank test) go to global memory.
+// Dataflow, no CTA-wide barrier in the sweep: a group of TPC threads owns
+// column c.  It waits for reflectors 0..c-1 in order (one mbarrier per
+// reflector, completed by the TPC threads of the group that formed it),
+// applies each to its column, and — with the sub-diagonal norm accumulated
+// inside the last update — forms reflector c (dlarfg) and arrives on its
+// mbarrier.  The critical path per reflector is therefore one column
+// update + one dlarfg; every other column catches up off that path.
+// Reflectors stay unscaled during the sweep (the 1/(alpha-beta) factor is
+// folded into the dot and the update) and are scaled once at the end.
+template <int TPC>
+__device__ inline double group_sum(double v) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned mask = (TPC == 32 ? 0xffffffffu : ((1u << TPC) - 1u) << (lane & ~(TPC - 1)));
+#pragma unroll
+    for (int off = 1; off < TPC; off <<= 1) v += __shfl_xor_sync(mask, v, off);
+    return v;
+}
+
+// dlarfg on a column whose alpha = col[j] and sub-diagonal sum of squares
+// `part` are known; writes tau, scal = 1/(alpha-beta) and beta into col[j].
+__device__ inline void dlarfg(double *col, int j, double part, double *tau_out,
+                              double *scal_out) {
+    const double alpha = col[j];
+    double t = 0.0, scal = 0.0;
+    if (part > 0.0) {
+        const double beta = -copysign(sqrt(__fma_rn(alpha, alpha, part)), alpha);
+        t = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+        col[j] = beta;
+    }
+    *tau_out = t;
+    *scal_out = scal;
+}
+
+template <int TPC>
+__global__ void __launch_bounds__(1024, 1) qr_kernel(const double *__restrict__ mT, int k1,
+                                                     int k2, int64_t ldm,
+                                                     double *__restrict__ qa,
+                                                     double *__restrict__ qtau,
+                                                     double *__restrict__ rrow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ld = k2 | 1;
-    double *A = reinterpret_cast<double *>(smem_raw);  // column c: A[c*ld + r] = M[r][c]
-    __shared__ double s_tau, s_scal;
-    const int tid = threadIdx.x, lane = tid & 31;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);           // k1 mbarriers
+    double *s_tau = reinterpret_cast<double *>(smem_raw) + k1;        // k1
+    double *s_scal = s_tau + k1;                                      // k1
+    double *A = s_scal + k1;  // column c: A[c*ld + r] = M[r][c]
+    const int tid = threadIdx.x;
+    const int c = tid / TPC, q = tid % TPC;
+    const unsigned gmask = (TPC == 32 ? 0xffffffffu
+                                      : ((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1)));
 
-    for (int i = tid; i < k1 * k2; i += blockDim.x) {
-        const int c = i / k2, r = i % k2;
-        A[c * ld + r] = mT[(int64_t)c * ldm + r];
+    {  // stage M (loads batched 8 deep: the copy is L2-latency bound)
+        const int n = k1 * k2;
+        for (int i0 = tid; i0 < n; i0 += 8 * blockDim.x) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                v[u] = i < n ? mT[(int64_t)(i / k2) * ldm + i % k2] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < n) A[(i / k2) * ld + i % k2] = v[u];
+            }
+        }
+    }
+    for (int i = tid; i < k1; i += blockDim.x) mbar_init(bar + i, TPC);
+    __syncthreads();
+
+    if (c < k1) {
+        double *colc = A + (size_t)c * ld;
+        double part0 = 0.0, part1 = 0.0;
+        if (c == 0)
+            for (int r = 1 + q; r < k2; r += TPC) part0 = __fma_rn(colc[r], colc[r], part0);
+        for (int j = 0; j < c; ++j) {
+            mbar_wait(bar + j, 0);
+            const double tj = s_tau[j], scal = s_scal[j];
+            const bool last = j == c - 1;
+            if (last) QR_T(c, 0);
+            if (tj == 0.0) {
+                if (last)
+                    for (int r = c + 1 + q; r < k2; r += TPC) part0 = __fma_rn(colc[r], colc[r], part0);
+                continue;
+            }
+            const double *colj = A + (size_t)j * ld;
+            // w = v^T A[:,c] with v_j = 1, v_r = scal * colj[r]
+            double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+            int r = j + 1 + q;
+            for (; r + 3 * TPC < k2; r += 4 * TPC) {
+                const double a0 = colj[r], a1 = colj[r + TPC], a2 = colj[r + 2 * TPC],
+                             a3 = colj[r + 3 * TPC];
+                const double b0 = colc[r], b1 = colc[r + TPC], b2 = colc[r + 2 * TPC],
+                             b3 = colc[r + 3 * TPC];
+                w0 = __fma_rn(a0, b0, w0);
+                w1 = __fma_rn(a1, b1, w1);
+                w2 = __fma_rn(a2, b2, w2);
+                w3 = __fma_rn(a3, b3, w3);
+            }
+            for (; r < k2; r += TPC) w0 = __fma_rn(colj[r], colc[r], w0);
+            const double dot = group_sum<TPC>((w0 + w1) + (w2 + w3));
+            if (last) QR_T(c, 1);
+            const double f = tj * __fma_rn(scal, dot, colc[j]);
+            const double fs = f * scal;
+            __syncwarp(gmask);  // every lane has read colc[j]
+            if (q == 0) colc[j] -= f;
+            r = j + 1 + q;
+            for (; r + 3 * TPC < k2; r += 4 * TPC) {
+                const double a0 = colj[r], a1 = colj[r + TPC], a2 = colj[r + 2 * TPC],
+                             a3 = colj[r + 3 * TPC];
+                const double b0 = colc[r], b1 = colc[r + TPC], b2 = colc[r + 2 * TPC],
+                             b3 = colc[r + 3 * TPC];
+                const double n0 = __fma_rn(-fs, a0, b0), n1 = __fma_rn(-fs, a1, b1),
+                             n2 = __fma_rn(-fs, a2, b2), n3 = __fma_rn(-fs, a3, b3);
+                colc[r] = n0;
+                colc[r + TPC] = n1;
+                colc[r + 2 * TPC] = n2;
+                colc[r + 3 * TPC] = n3;
+                if (last) {
+                    part0 = __fma_rn(n0, r == c ? 0.0 : n0, part0);
+                    part1 = __fma_rn(n1, n1, part1);
+                    part0 = __fma_rn(n2, n2, part0);
+                    part1 = __fma_rn(n3, n3, part1);
+                }
+            }
+            for (; r < k2; r += TPC) {
+                const double nv = __fma_rn(-fs, colj[r], colc[r]);
+                colc[r] = nv;
+                if (last) part0 = __fma_rn(nv, r == c ? 0.0 : nv, part0);
+            }
+        }
+        // reflector c
+        QR_T(c, 2);
+        const double part = group_sum<TPC>(part0 + part1);
+        QR_T(c, 3);
+        if (q == 0) dlarfg(colc, c, part, s_tau + c, s_scal + c);
+        QR_T(c, 4);
+        mbar_arrive(bar + c);
     }
     __syncthreads();
-    for (int j = 0; j < k1; ++j) {
-        double *colj = A + j * ld;
-        if (tid < 32) {  // dlarfg on column j (warp 0)
-            double part = 0.0;
-            for (int r = j + 1 + lane; r < k2; r += 32) part += colj[r] * colj[r];
-#pragma unroll
-            for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-            if (lane == 0) {
-                const double alpha = colj[j];
-                double t = 0.0, scal = 0.0;
-                if (part > 0.0) {
-                    const double beta = -copysign(hypot(alpha, sqrt(part)), alpha);
-                    t = (beta - alpha) / beta;
-                    scal = 1.0 / (alpha - beta);
-                    colj[j] = beta;
-                }
-                s_tau = t;
-                s_scal = scal;
-                qtau[j] = t;
-            }
-        }
-        __syncthreads();
-        const double tj = s_tau, scal = s_scal;
-        if (tj != 0.0) {
-            // 4 threads per trailing column c: w = v^T A[:,c] (v_j = 1,
-            // v_r = scal*colj[r]), quad-shuffle reduction, then the update
-            const int q = tid & 3;
-            for (int c = j + 1 + (tid >> 2); c < k1; c += blockDim.x >> 2) {
-                double *colc = A + c * ld;
-                double w0 = q == 0 ? colc[j] : 0.0, w1 = 0.0;
-                int r = j + 1 + q;
-                for (; r + 4 < k2; r += 8) {
-                    w0 = __fma_rn(colj[r] * scal, colc[r], w0);
-                    w1 = __fma_rn(colj[r + 4] * scal, colc[r + 4], w1);
-                }
-                for (; r < k2; r += 4) w0 = __fma_rn(colj[r] * scal, colc[r], w0);
-                double w = w0 + w1;
-                const unsigned qmask = 0xFu << ((threadIdx.x & 31) & ~3);  // the quad
-                w += __shfl_xor_sync(qmask, w, 1);
-                w += __shfl_xor_sync(qmask, w, 2);
-                const double f = tj * w;
-                if (q == 0) colc[j] -= f;
-                for (int rr = j + 1 + q; rr < k2; rr += 4) colc[rr] = __fma_rn(-f, colj[rr] * scal, colc[rr]);
-            }
-        }
-        __syncthreads();
-        if (tj != 0.0)
-            for (int r = j + 1 + tid; r < k2; r += blockDim.x) colj[r] *= scal;
-        __syncthreads();
+    for (int i = tid; i < k1; i += blockDim.x) qtau[i] = s_tau[i];
+    // scale the stored reflectors: v_r = scal_j * u_r below the diagonal
+    for (int i = tid; i < k1 * ld; i += blockDim.x) {
+        const int cc = i / ld, r = i % ld;
+        double v = A[i];
+        if (r > cc && r < k2 && s_tau[cc] != 0.0) v *= s_scal[cc];
+        qa[i] = v;
     }
-    for (int i = tid; i < k1 * ld; i += blockDim.x) qa[i] = A[i];
     for (int i = tid; i < k1 * k1; i += blockDim.x) {  // R row-major (for the rank test)
-        const int r = i / k1, c = i % k1;
-        rrow[i] = r <= c ? A[c * ld + r] : 0.0;
+        const int r = i / k1, cc = i % k1;
+        rrow[i] = r <= cc ? A[cc * ld + r] : 0.0;
     }
 }
 
-// Phase 2 (many CTAs): CTA 0 runs the rank test on R; every warp of the
-// other CTAs forms one column of pinv^T = (R^-1 Q^T)^T from the reflectors.
+// Phase 2 (many CTAs): every warp forms one column c of
+// pinv^T = (R^-1 Q^T)^T: z = Q^T e_c (the k1 reflectors in order), then the
+// back substitution R x = z[:k1].  The packed reflectors/R are staged in
+// each CTA's shared memory and z lives in the lanes' registers (lane l owns
+// rows r == l mod 32, PER per lane), so the 2·k1 sequential steps cost a
+// warp reduction or a shuffle broadcast each, never a global round trip.
+template <int PER>
 __global__ void __launch_bounds__(256) qr_tail_kernel(const double *__restrict__ qa,
                                                       const double *__restrict__ qtau, int k1,
                                                       int k2, double *__restrict__ pinvT,
-                                                      int64_t ldp, double *__restrict__ stats,
-                                                      const double *__restrict__ rrow) {
+                                                      int64_t ldp) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ld = k2 | 1;
+    double *V = reinterpret_cast<double *>(smem_raw);  // k1 x ld, as qa
+    double *tau = V + (size_t)k1 * ld;                  // qtau follows qa in the workspace
+    __shared__ uint64_t tbar;
+    (void)qtau;
+    if (threadIdx.x == 0) {
+        mbar_init(&tbar, 1);
+        fence_mbar_init();
+        // one bulk copy of reflectors + tau (rounded up to 16 B; the
+        // workspace has slack after tau)
+        const unsigned bytes = (unsigned)((sizeof(double) * ((size_t)k1 * ld + k1) + 15) & ~15ull);
+        mbar_arrive_expect_tx(&tbar, bytes);
+        bulk_g2s(V, qa, bytes, &tbar);
+    }
+    __syncthreads();
+    mbar_wait(&tbar, 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (c >= k2) return;
+    double z[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) z[i] = (i * 32 + lane == c) ? 1.0 : 0.0;
+    for (int j = 0; j < k1; ++j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const double *vj = V + (size_t)j * ld;
+        double w = 0.0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int r = i * 32 + lane;
+            const double v = r == j ? 1.0 : (r > j && r < k2 ? vj[r] : 0.0);
+            w = __fma_rn(v, z[i], w);
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
+        const double f = tj * w;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int r = i * 32 + lane;
+            const double v = r == j ? 1.0 : (r > j && r < k2 ? vj[r] : 0.0);
+            z[i] = __fma_rn(-f, v, z[i]);
+        }
+    }
+    // back substitution on the first k1 entries: R x = z
+    for (int r = k1 - 1; r >= 0; --r) {
+        const double *rc = V + (size_t)r * ld;  // column r of R (rows < r)
+        const int ro = r & 31, ri = r >> 5;
+        double zr = 0.0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if (i == ri) zr = z[i];
+        const double xr = __shfl_sync(0xffffffffu, zr, ro) / rc[r];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int q = i * 32 + lane;
+            if (q < r) z[i] = __fma_rn(-rc[q], xr, z[i]);
+            if (i == ri && lane == ro) z[i] = xr;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int q = i * 32 + lane;
+        if (q < k1) pinvT[(int64_t)c * ldp + q] = z[i];
+    }
+}
+
+// the same for any k2 (z in shared memory): used when k2 > 32 * kTailMaxPer
+__global__ void __launch_bounds__(256) qr_tail_any_kernel(const double *__restrict__ qa,
+                                                          const double *__restrict__ qtau,
+                                                          int k1, int k2,
+                                                          double *__restrict__ pinvT,
+                                                          int64_t ldp) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ld = k2 | 1;
     const int k2p = (k2 + 1) & ~1;
     double *sm = reinterpret_cast<double *>(smem_raw);
-    (void)stats;
-    (void)rrow;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = blockIdx.x * (blockDim.x >> 5) + warp;
     if (c >= k2) return;
@@ -426,7 +589,7 @@ __global__ void __launch_bounds__(256) dgemm_kernel(const double *__restrict__ A
 
 static size_t qr_pinv_smem(int64_t k1, int64_t k2) {
     const int64_t ld = k2 | 1;
-    return sizeof(double) * (size_t)(k1 * ld) + 64;
+    return sizeof(double) * (size_t)(k1 * ld + 3 * k1) + 64;
 }
 
 }  // namespace srlu
@@ -455,18 +618,36 @@ extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ld
     double *qa = (double *)ws;
     double *qtau = qa + (size_t)k1 * (k2 | 1);
     double *rrow = qtau + k1;
-    SRLU_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    qr_kernel<<<1, kQrThreads, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau, rrow);
+    {  // one group of 8 (k1 <= 128) or 4 threads per column
+        auto qr = k1 <= 128 ? qr_kernel<8> : qr_kernel<4>;
+        SRLU_REQUIRE(k1 <= 256, SRLU_ERR_UNSUPPORTED, "qr_pinv: k1 > 256");
+        SRLU_CUDA(cudaFuncSetAttribute(qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        qr<<<1, 1024, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau, rrow);
+    }
     SRLU_CHECK_LAUNCH("qr_kernel");
-    const int k2p = (int)((k2 + 1) & ~1);
-    size_t smem2 = sizeof(double) * (size_t)(8 * k2p + 64);
-    size_t smem_rank = sizeof(double) * (size_t)(3 * k2p + 64);
-    if (smem_rank > smem2) smem2 = smem_rank;
-    SRLU_CUDA(cudaFuncSetAttribute(qr_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem2));
-    qr_tail_kernel<<<(unsigned)ceil_div(k2, 8), 256, smem2, s>>>(qa, qtau, (int)k1, (int)k2,
-                                                                       pinvT, ldp, stats, rrow);
+    const unsigned tail_grid = (unsigned)ceil_div(k2, 8);
+    const size_t smem_v = sizeof(double) * (size_t)(k1 * (k2 | 1) + k1) + 64;  // +16 B round-up
+    auto tail = [&](auto kern) -> int {
+        SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_v));
+        kern<<<tail_grid, 256, smem_v, s>>>(qa, qtau, (int)k1, (int)k2, pinvT, ldp);
+        return SRLU_OK;
+    };
+    int rc;
+    if (k2 <= 32) rc = tail(qr_tail_kernel<1>);
+    else if (k2 <= 64) rc = tail(qr_tail_kernel<2>);
+    else if (k2 <= 128) rc = tail(qr_tail_kernel<4>);
+    else if (k2 <= 192) rc = tail(qr_tail_kernel<6>);
+    else if (k2 <= 32 * kTailMaxPer) rc = tail(qr_tail_kernel<kTailMaxPer>);
+    else {
+        const size_t smem2 = sizeof(double) * (size_t)(8 * ((k2 + 1) & ~1) + 64);
+        SRLU_REQUIRE(smem2 <= 200 * 1024, SRLU_ERR_UNSUPPORTED, "qr_pinv: k2 too large");
+        SRLU_CUDA(cudaFuncSetAttribute(qr_tail_any_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        qr_tail_any_kernel<<<tail_grid, 256, smem2, s>>>(qa, qtau, (int)k1, (int)k2, pinvT, ldp);
+        rc = SRLU_OK;
+    }
+    if (rc != SRLU_OK) return rc;
     SRLU_CHECK_LAUNCH("qr_tail_kernel");
     return SRLU_OK;
 }

@@ -169,6 +169,28 @@ def test_lu_col_pivot_panels_bit_exact(P, k, n, seed):
     np.testing.assert_array_equal(r.U.numpy(), up)
 
 
+@pytest.mark.parametrize("m,k,seed", [(16384, 110, 8), (6000, 150, 2), (2048, 60, 9)])
+def test_lu_cluster_and_grid_variants_agree(P, m, k, seed, monkeypatch):
+    """Shapes that fit one cluster run the DSMEM-exchange kernel; the same
+    input through the 148-CTA grid kernel (SRLU_LU_NO_CLUSTER=1) and the
+    oracle must give identical P, L, U (row) and Q, L, U (col)."""
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(seed))
+    b = g.standard_normal((m, k))
+    perm, lo, up = O.lu_row_pivot(b)
+    q, lo2, up2 = O.lu_col_pivot(b.T.copy())
+    for no_cluster in ("0", "1"):
+        monkeypatch.setenv("SRLU_LU_NO_CLUSTER", no_cluster)
+        r = P.lu_row_pivot(b)
+        np.testing.assert_array_equal(r.P.indices, perm, err_msg=no_cluster)
+        np.testing.assert_array_equal(r.L.numpy(), lo, err_msg=no_cluster)
+        np.testing.assert_array_equal(r.U.numpy(), up, err_msg=no_cluster)
+        c = P.lu_col_pivot(b.T.copy())
+        np.testing.assert_array_equal(c.Q.indices, q, err_msg=no_cluster)
+        np.testing.assert_array_equal(c.L.numpy(), lo2, err_msg=no_cluster)
+        np.testing.assert_array_equal(c.U.numpy(), up2, err_msg=no_cluster)
+
+
 def test_lu_low_rank_threshold_path(P):
     """Exactly low rank: later pivots fall under PIVOT_RTOL*||B||_F."""
     from oracle import randlu as O
