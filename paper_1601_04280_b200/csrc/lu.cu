@@ -425,6 +425,17 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned addr, unsigned parity
         : "memory");
 }
 
+// warp argmax of (a desc, key asc) with three redux.sync steps: max of the
+// high word, max of the low word among those, min key among the maxima
+__device__ __forceinline__ void warp_argmax_redux(unsigned long long &a, unsigned &key) {
+    const unsigned hi = (unsigned)(a >> 32), lo = (unsigned)a;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    const bool top = hi == mhi && lo == mlo;
+    key = __reduce_min_sync(0xffffffffu, top ? key : 0xFFFFFFFFu);
+    a = ((unsigned long long)mhi << 32) | mlo;
+}
+
 struct LuClusterParams {
     LuParams p;
     double *wt;   // k x ldt attribute-major working copy
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
     __shared__ unsigned s_bkey[2];
     __shared__ double s_wsum[32];
     __shared__ double s_thresh;
-    __shared__ __align__(8) uint64_t xbar[2];
+    __shared__ __align__(8) uint64_t xbar[3];
 
     const LuParams &p = cp.p;
     double *const wt = cp.wt;
@@ -458,9 +469,9 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
     const bool mine = tid < ne;  // thread tid owns entity e0 + tid
     const int64_t me = e0 + tid;
 
-    double *xrow = reinterpret_cast<double *>(smem_raw);     // [2][CL][b2]
-    Cand *xcand = reinterpret_cast<Cand *>(xrow + (size_t)2 * CL * b2);  // [2][CL]
-    double *xpart = reinterpret_cast<double *>(xcand + 2 * CL);          // [CL]
+    double *xrow = reinterpret_cast<double *>(smem_raw);     // [3][CL][b2]
+    Cand *xcand = reinterpret_cast<Cand *>(xrow + (size_t)3 * CL * b2);  // [3][CL]
+    double *xpart = reinterpret_cast<double *>(xcand + 3 * CL);          // [CL]
     double *ucol = xpart + CL;                                           // [32][b]
     double *PR = ucol + 32 * b;                                          // b x b
     double *Ach = PR + (((size_t)b * b + 1) & ~(size_t)1);               // b x AW (16-B aligned)
@@ -474,23 +485,13 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
 
     // CTA argmax of (|w| desc, position asc); key = pos << 10 | local entity
     auto cta_argmax = [&](unsigned long long a, unsigned key, int par) {
-#pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            const unsigned long long oa = __shfl_xor_sync(0xffffffffu, a, off);
-            const unsigned ok = __shfl_xor_sync(0xffffffffu, key, off);
-            if (better(oa, ok, a, key)) { a = oa; key = ok; }
-        }
+        warp_argmax_redux(a, key);
         if (lane == 0) { s_wabs[par][warp] = a; s_wkey[par][warp] = key; }
         __syncthreads();
         if (warp == 0) {
             a = lane < nwarps ? s_wabs[par][lane] : 0ULL;
             key = lane < nwarps ? s_wkey[par][lane] : 0xFFFFFFFFu;
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                const unsigned long long oa = __shfl_xor_sync(0xffffffffu, a, off);
-                const unsigned ok = __shfl_xor_sync(0xffffffffu, key, off);
-                if (better(oa, ok, a, key)) { a = oa; key = ok; }
-            }
+            warp_argmax_redux(a, key);
             if (lane == 0) { s_babs[par] = a; s_bkey[par] = key; }
         }
         __syncthreads();
@@ -501,12 +502,46 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
         const int bw_s = min(b, k - (st / b) * b);
         return (unsigned)(CL * (((bw_s + 1) >> 1) * 16 + 16));
     };
+    // push step st's CTA candidate (computed by cta_argmax into par st&1) and
+    // its panel row into slot st%3 of every CTA: the owner's warp does it
+    auto push = [&](int st, int bw_s) {
+        const int par = st & 1;
+        const unsigned long long babs = s_babs[par];
+        const unsigned bkey = s_bkey[par];
+        const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);
+        if (warp != (owner >= 0 ? owner >> 5 : 0)) return;
+        __syncwarp();
+        const int sl = st % 3;
+        const int npair = (bw_s + 1) >> 1;
+        const unsigned pos = owner >= 0 ? (bkey >> 10) : 0xFFFFFFFFu;
+        const int ent = owner >= 0 ? (int)(e0 + owner) : -1;
+        // lanes d and d+16 serve destination d: the first half of the pairs,
+        // then the second half plus the candidate (mapa once per lane)
+        const unsigned dst = (unsigned)(lane & 15);
+        if ((int)dst < CL) {
+            const unsigned rbar = mapa_rank(smem_u32(&xbar[sl]), dst);
+            const unsigned rrow = mapa_rank(smem_u32(xrow + ((size_t)sl * CL + rank) * b2), dst);
+            const int half = (npair + 1) >> 1;
+            const int i0 = lane < 16 ? 0 : half, i1 = lane < 16 ? half : npair;
+            const double *src = panel + (size_t)(owner >= 0 ? owner : 0) * bs;
+            for (int it = i0; it < i1; ++it) {
+                const int x = 2 * it;
+                double v0 = 0.0, v1 = 0.0;
+                if (owner >= 0) {
+                    v0 = src[x];
+                    v1 = x + 1 < bw_s ? src[x + 1] : 0.0;
+                }
+                st_async_f64x2(rrow + 16u * (unsigned)it, v0, v1, rbar);
+            }
+            if (lane >= 16)
+                st_async_u64x2(mapa_rank(smem_u32(xcand + sl * CL + rank), dst), babs,
+                               ((unsigned long long)(unsigned)ent << 32) | pos, rbar);
+        }
+    };
     if (tid == 0) {
-        mbar_init_cta(smem_u32(&xbar[0]), 1u);
-        mbar_init_cta(smem_u32(&xbar[1]), 1u);
+        for (int i = 0; i < 3; ++i) mbar_init_cta(smem_u32(&xbar[i]), 1u);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_arrive_expect_tx_cta(smem_u32(&xbar[0]), step_bytes(0));
-        if (k > 1) mbar_arrive_expect_tx_cta(smem_u32(&xbar[1]), step_bytes(1));
+        for (int i = 0; i < 3 && i < k; ++i) mbar_arrive_expect_tx_cta(smem_u32(&xbar[i]), step_bytes(i));
     }
     // ---- transpose own entities into wt (through shared-memory tiles, full
     // 128-byte rows read by 16 consecutive threads); ||w||_F^2 on the way ----
@@ -561,68 +596,37 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
                 key = ((unsigned)mypos << 10) | (unsigned)tid;
             }
             cta_argmax(a, key, J & 1);
+            push(J, bw);
         }
         LU_T(6);
 
         for (int ls = 0; ls < bw; ++ls) {
             const int s = J + ls;
-            const int slot = s & 1;
-            // 1. warp d pushes {candidate, its panel row} into CTA d's slot
-            if (warp < CL) {
-                const unsigned long long babs = s_babs[slot];
-                const unsigned bkey = s_bkey[slot];
-                const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);
-                const unsigned dst = (unsigned)warp;
-                const int npair = (bw + 1) >> 1;
-                if (lane < npair) {
-                    const int x = 2 * lane;
-                    double v0 = 0.0, v1 = 0.0;
-                    if (owner >= 0) {
-                        v0 = panel[(size_t)owner * bs + x];
-                        v1 = x + 1 < bw ? panel[(size_t)owner * bs + x + 1] : 0.0;
-                    }
-                    st_async_f64x2(
-                        mapa_rank(smem_u32(xrow + ((size_t)slot * CL + rank) * b2 + x), dst), v0, v1,
-                        mapa_rank(smem_u32(&xbar[slot]), dst));
-                } else if (lane == 31) {
-                    const unsigned pos = owner >= 0 ? (bkey >> 10) : 0xFFFFFFFFu;
-                    const int ent = owner >= 0 ? (int)(e0 + owner) : -1;
-                    st_async_u64x2(mapa_rank(smem_u32(xcand + slot * CL + rank), dst), babs,
-                                   ((unsigned long long)(unsigned)ent << 32) | pos,
-                                   mapa_rank(smem_u32(&xbar[slot]), dst));
-                }
-            }
-            LU_T(1);
-            // 2. wait for the CL pushes of this step
-            mbar_wait_cluster(smem_u32(&xbar[slot]), (unsigned)((s >> 1) & 1));
-            // re-arm this slot for step s+2 (its data can only arrive after
-            // this CTA's own step-(s+1) push, which follows in program order)
-            if (tid == 0 && s + 2 < k) mbar_arrive_expect_tx_cta(smem_u32(&xbar[slot]), step_bytes(s + 2));
+            const int sl = s % 3;
+            // 1. wait for the CL pushes of this step; re-arm the slot for s+3
+            //    (its data can only arrive after this CTA's push of step s+2)
+            mbar_wait_cluster(smem_u32(&xbar[sl]), (unsigned)((s / 3) & 1));
+            if (tid == 0 && s + 3 < k) mbar_arrive_expect_tx_cta(smem_u32(&xbar[sl]), step_bytes(s + 3));
             LU_T(2);
-            // 3. winner: every warp reduces the CL candidates itself
+            // 2. winner: every warp reduces the CL candidates itself
             unsigned long long ga = 0ULL;
             unsigned gkey = 0xFFFFFFFFu;
             if (lane < CL) {
-                const Cand c = xcand[slot * CL + lane];
+                const Cand c = xcand[sl * CL + lane];
                 if (c.entity >= 0) { ga = c.absbits; gkey = (c.pos << 4) | (unsigned)lane; }
             }
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ga, off);
-                const unsigned ok = __shfl_xor_sync(0xffffffffu, gkey, off);
-                if (better(oa, ok, ga, gkey)) { ga = oa; gkey = ok; }
-            }
+            warp_argmax_redux(ga, gkey);
             const int gc = (int)(gkey & 15u);
             const int wpos = (int)(gkey >> 4);
-            const int went = xcand[slot * CL + gc].entity;
-            const double *u = xrow + ((size_t)slot * CL + gc) * b2;
+            const int went = xcand[sl * CL + gc].entity;
+            const double *u = xrow + ((size_t)sl * CL + gc) * b2;
             const double pivv = u[ls];
             const bool big = fabs(pivv) > thresh;
             if (tid == 0) pw_ent[ls] = went;
             if (b < k && tid < bw)
                 PR[ls * b + tid] = (MODE == MODE_COL && tid > ls) ? (big ? u[tid] / pivv : 0.0)
                                                                   : u[tid];
-            // 4. swap positions s <-> wpos (own entity only)
+            // swap positions s <-> wpos (own entity only)
             if (mine) {
                 if (mypos == s) mypos = wpos;
                 if (me == went) mypos = s;
@@ -635,15 +639,18 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
                 um = uw;
             }
             LU_T(3);
-            // 5. update own panel row (next pivot column first)
+            // 3. critical path: the next pivot column of own entity only
+            double lm = 0.0;
+            bool rest = false;  // the rest of the panel row still to update
             if (mine) {
                 if (MODE == MODE_ROW) {
                     if (mypos > s) {
                         if (big) {
-                            const double lm = myrow[ls] / pivv;
+                            lm = myrow[ls] / pivv;
                             myrow[ls] = lm;
-                            for (int x = ls + 1; x < bw; ++x)
-                                myrow[x] = __dsub_rn(myrow[x], __dmul_rn(lm, u[x]));
+                            if (ls + 1 < bw)
+                                myrow[ls + 1] = __dsub_rn(myrow[ls + 1], __dmul_rn(lm, u[ls + 1]));
+                            rest = true;
                         } else {
                             myrow[ls] = 0.0;
                         }
@@ -652,14 +659,35 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
                     if (me == went) {
                         for (int x = ls + 1; x < bw; ++x) myrow[x] = um[x];
                     } else if (mypos > s && big) {
-                        const double lm = myrow[ls];
-                        for (int x = ls + 1; x < bw; ++x)
-                            myrow[x] = __dsub_rn(myrow[x], __dmul_rn(um[x], lm));
+                        lm = myrow[ls];
+                        if (ls + 1 < bw)
+                            myrow[ls + 1] = __dsub_rn(myrow[ls + 1], __dmul_rn(um[ls + 1], lm));
+                        rest = true;
                     }
                 }
             }
+            // x = ls+2 .. bw-1 in batches of 8 (loads first: no store-to-load
+            // dependence between iterations)
+            auto finish_row = [&]() {
+                for (int x0 = ls + 2; x0 < bw; x0 += 8) {
+                    double r[8], w[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const bool in = x0 + i < bw;
+                        r[i] = in ? myrow[x0 + i] : 0.0;
+                        w[i] = in ? (MODE == MODE_ROW ? u[x0 + i] : um[x0 + i]) : 0.0;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (x0 + i < bw)
+                            myrow[x0 + i] = MODE == MODE_ROW ? __dsub_rn(r[i], __dmul_rn(lm, w[i]))
+                                                             : __dsub_rn(r[i], __dmul_rn(w[i], lm));
+                }
+            };
             LU_T(4);
             if (ls + 1 < bw) {
+                // 4. CTA argmax of the next column; its owner completes its row
+                //    and its warp pushes step s+1 before anyone else's row work
                 unsigned long long a = 0ULL;
                 unsigned key = 0xFFFFFFFFu;
                 if (mine && mypos >= s + 1) {
@@ -667,7 +695,16 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
                     key = ((unsigned)mypos << 10) | (unsigned)tid;
                 }
                 cta_argmax(a, key, (s + 1) & 1);
+                const unsigned bkey = s_bkey[(s + 1) & 1];
+                if (rest && bkey != 0xFFFFFFFFu && (int)(bkey & 1023u) == tid) {
+                    finish_row();
+                    rest = false;
+                }
+                push(s + 1, bw);
             }
+            LU_T(1);
+            // 5. the rest of the panel row (overlaps the exchange of step s+1)
+            if (rest) finish_row();
             LU_T(0);
         }
         __syncthreads();  // PR / pw_ent complete
@@ -775,9 +812,793 @@ __global__ void __launch_bounds__(1024, 1) lu_cluster_kernel(LuClusterParams cp)
 static size_t lu_cluster_smem_bytes(int rpc, int b, int bs, int CL, int k) {
     const int AW = ((k > b ? k - b : 1) + 15) & ~15;
     const int b2 = (b + 1) & ~1;
-    return sizeof(double) * ((size_t)2 * CL * b2 + CL + (size_t)32 * b + (((size_t)b * b + 1) & ~(size_t)1) +
+    return sizeof(double) * ((size_t)3 * CL * b2 + CL + (size_t)32 * b + (((size_t)b * b + 1) & ~(size_t)1) +
                              (size_t)b * AW + (size_t)rpc * bs) +
-           sizeof(Cand) * 2 * CL + sizeof(int) * ((size_t)b + rpc) + 16;
+           sizeof(Cand) * 3 * CL + sizeof(int) * ((size_t)b + rpc) + 16;
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident cluster LU (the default cluster path): as above, but the
+// panel width is a compile-time B <= 16 and each thread keeps its entity's
+// panel row in registers, so a pivot step's row update is B predicated
+// mul/sub pairs against the pivot row (128-bit broadcast loads) with no
+// shared-memory traffic for the rows.  The shared-memory row kernel above
+// spent most of each step in shared-memory bandwidth (row loads/stores),
+// which also delayed the remote st.async deliveries of the exchange.
+template <int B>
+__device__ __forceinline__ double rsel(const double (&r)[B], int i) {
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+        if (j == i) v = r[j];
+    return v;
+}
+
+constexpr int kLuTile = 16;  // transpose tile width (row stride kLuTile + 1)
+
+template <int MODE, int B>
+__global__ void __launch_bounds__(1024, 1) lu_cluster_reg_kernel(LuClusterParams cp) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ unsigned long long s_wabs[2][32];
+    __shared__ unsigned s_wkey[2][32];
+    __shared__ unsigned long long s_babs[2];
+    __shared__ unsigned s_bkey[2];
+    __shared__ double s_wsum[32];
+    __shared__ double s_thresh;
+    __shared__ __align__(8) uint64_t xbar[3];
+    __shared__ __align__(16) double s_own[B];
+
+    const LuParams &p = cp.p;
+    double *const wt = cp.wt;
+    const int64_t ldt = cp.ldt;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int CL = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int k = p.k, rpc = p.rpc;
+    const int b = k < B ? k : B;
+    const int AW = ((k > b ? k - b : 1) + 15) & ~15;
+    const int64_t e0 = (int64_t)rank * rpc;
+    const int ne = (int)max((int64_t)0, min((int64_t)rpc, p.M - e0));
+    const bool mine = tid < ne;
+    const int64_t me = e0 + tid;
+
+    double *xrow = reinterpret_cast<double *>(smem_raw);                 // [3][CL][B]
+    Cand *xcand = reinterpret_cast<Cand *>(xrow + (size_t)3 * CL * B);   // [3][CL]
+    double *xpart = reinterpret_cast<double *>(xcand + 3 * CL);          // [CL]
+    double *ucol = xpart + ((CL + 1) & ~1);                              // [32][B]
+    double *PR = ucol + 32 * B;                                          // B x B
+    double *Ach = PR + B * B;                                            // B x AW
+    double *tile = Ach + (size_t)B * AW;                                 // rpc x (kLuTile+1)
+    int *pw_ent = reinterpret_cast<int *>(tile + (size_t)rpc * (kLuTile + 1));  // B
+    int *qarr = pw_ent + B;                                              // rpc
+    double *mytile = tile + (size_t)tid * (kLuTile + 1);
+    int mypos = (int)me;
+    double r[B];
+
+    auto cta_argmax = [&](unsigned long long a, unsigned key, int par) {
+        warp_argmax_redux(a, key);
+        if (lane == 0) { s_wabs[par][warp] = a; s_wkey[par][warp] = key; }
+        __syncthreads();
+        if (warp == 0) {
+            a = lane < nwarps ? s_wabs[par][lane] : 0ULL;
+            key = lane < nwarps ? s_wkey[par][lane] : 0xFFFFFFFFu;
+            warp_argmax_redux(a, key);
+            if (lane == 0) { s_babs[par] = a; s_bkey[par] = key; }
+        }
+        __syncthreads();
+    };
+    auto step_bytes = [&](int st) -> unsigned {
+        const int bw_s = min(b, k - (st / b) * b);
+        return (unsigned)(CL * (((bw_s + 1) >> 1) * 16 + 16));
+    };
+    // after cta_argmax(.., st&1): the owner stages its row, its warp pushes
+    // {candidate, row} into slot st%3 of every CTA (lanes d, d+16 -> CTA d)
+    auto stage_and_push = [&](int st, int bw_s) {
+        const int par = st & 1;
+        const unsigned long long babs = s_babs[par];
+        const unsigned bkey = s_bkey[par];
+        const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);
+        if (warp != (owner >= 0 ? owner >> 5 : 0)) return;
+        if (tid == owner) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) s_own[i] = r[i];
+        }
+        __syncwarp();
+        const int sl = st % 3;
+        const int npair = (bw_s + 1) >> 1;
+        const unsigned pos = owner >= 0 ? (bkey >> 10) : 0xFFFFFFFFu;
+        const int ent = owner >= 0 ? (int)(e0 + owner) : -1;
+        const unsigned dst = (unsigned)(lane & 15);
+        if ((int)dst < CL) {
+            const unsigned rbar = mapa_rank(smem_u32(&xbar[sl]), dst);
+            const unsigned rrow = mapa_rank(smem_u32(xrow + ((size_t)sl * CL + rank) * B), dst);
+            const int half = (npair + 1) >> 1;
+            const int i0 = lane < 16 ? 0 : half, i1 = lane < 16 ? half : npair;
+            for (int it = i0; it < i1; ++it) {
+                const int x = 2 * it;
+                const double v0 = owner >= 0 ? s_own[x] : 0.0;
+                const double v1 = owner >= 0 && x + 1 < bw_s ? s_own[x + 1] : 0.0;
+                st_async_f64x2(rrow + 16u * (unsigned)it, v0, v1, rbar);
+            }
+            if (lane >= 16)
+                st_async_u64x2(mapa_rank(smem_u32(xcand + sl * CL + rank), dst), babs,
+                               ((unsigned long long)(unsigned)ent << 32) | pos, rbar);
+        }
+    };
+
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init_cta(smem_u32(&xbar[i]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 3 && i < k; ++i) mbar_arrive_expect_tx_cta(smem_u32(&xbar[i]), step_bytes(i));
+    }
+    // ---- transpose own entities into wt through shared-memory tiles;
+    // ||w||_F^2 on the way (per entity in column order) ----
+    double ss = 0.0;
+    for (int x0 = 0; x0 < k; x0 += kLuTile) {
+        const int cw = min(kLuTile, k - x0);
+        for (int t = tid; t < ne * kLuTile; t += blockDim.x) {
+            const int e = t / kLuTile, c = t % kLuTile;
+            if (c < cw) tile[(size_t)e * (kLuTile + 1) + c] = p.w[(e0 + e) * p.ld + x0 + c];
+        }
+        __syncthreads();
+        if (mine)
+            for (int c = 0; c < cw; ++c) {
+                const double v = mytile[c];
+                wt[(int64_t)(x0 + c) * ldt + me] = v;
+                ss += v * v;
+            }
+        __syncthreads();
+    }
+    cl.sync();  // barriers initialised, every CTA running, before any remote access
+    {  // thresh = PIVOT_RTOL * ||w||_F (fixed-order two-level sum)
+#pragma unroll
+        for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        if (lane == 0) s_wsum[warp] = ss;
+        __syncthreads();
+        if (warp == 0) {
+            double v = lane < nwarps ? s_wsum[lane] : 0.0;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane < CL) *cl.map_shared_rank(xpart + rank, lane) = v;
+        }
+        cl.sync();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int c = 0; c < CL; ++c) tot += xpart[c];
+            s_thresh = kPivotRtol * sqrt(tot);
+        }
+        __syncthreads();
+    }
+    const double thresh = s_thresh;
+    LU_T0();
+
+    for (int J = 0; J < k; J += b) {
+        const int bw = min(b, k - J);
+#pragma unroll
+        for (int i = 0; i < B; ++i) r[i] = (mine && i < bw) ? wt[(int64_t)(J + i) * ldt + me] : 0.0;
+        {
+            unsigned long long a = 0ULL;
+            unsigned key = 0xFFFFFFFFu;
+            if (mine && mypos >= J) {
+                a = (unsigned long long)__double_as_longlong(fabs(r[0]));
+                key = ((unsigned)mypos << 10) | (unsigned)tid;
+            }
+            cta_argmax(a, key, J & 1);
+            stage_and_push(J, bw);
+        }
+        LU_T(6);
+
+        for (int ls = 0; ls < bw; ++ls) {
+            const int s = J + ls;
+            const int sl = s % 3;
+            mbar_wait_cluster(smem_u32(&xbar[sl]), (unsigned)((s / 3) & 1));
+            if (tid == 0 && s + 3 < k) mbar_arrive_expect_tx_cta(smem_u32(&xbar[sl]), step_bytes(s + 3));
+            LU_T(2);
+            unsigned long long ga = 0ULL;
+            unsigned gkey = 0xFFFFFFFFu;
+            if (lane < CL) {
+                const Cand c = xcand[sl * CL + lane];
+                if (c.entity >= 0) { ga = c.absbits; gkey = (c.pos << 4) | (unsigned)lane; }
+            }
+            warp_argmax_redux(ga, gkey);
+            const int gc = (int)(gkey & 15u);
+            const int wpos = (int)(gkey >> 4);
+            const int went = xcand[sl * CL + gc].entity;
+            const double *u = xrow + ((size_t)sl * CL + gc) * B;
+            const double pivv = u[ls];
+            const bool big = fabs(pivv) > thresh;
+            if (tid == 0) pw_ent[ls] = went;
+            if (b < k && tid < bw)
+                PR[ls * B + tid] = (MODE == MODE_COL && tid > ls) ? (big ? u[tid] / pivv : 0.0)
+                                                                  : u[tid];
+            if (mine) {
+                if (mypos == s) mypos = wpos;
+                if (me == went) mypos = s;
+            }
+            const double *um = u;
+            if (MODE == MODE_COL) {
+                double *uw = ucol + warp * B;
+                if (lane > ls && lane < bw) uw[lane] = big ? u[lane] / pivv : 0.0;
+                __syncwarp();
+                um = uw;
+            }
+            LU_T(3);
+            if (mine) {
+                const double2 *uv = reinterpret_cast<const double2 *>(um);
+                if (MODE == MODE_ROW) {
+                    if (mypos > s) {
+                        if (big) {
+                            const double lm = rsel<B>(r, ls) / pivv;
+#pragma unroll
+                            for (int i2 = 0; i2 < B / 2; ++i2) {
+                                const double2 w = uv[i2];
+                                const int i = 2 * i2;
+                                if (i == ls) r[i] = lm;
+                                else if (i > ls && i < bw) r[i] = __dsub_rn(r[i], __dmul_rn(lm, w.x));
+                                if (i + 1 == ls) r[i + 1] = lm;
+                                else if (i + 1 > ls && i + 1 < bw)
+                                    r[i + 1] = __dsub_rn(r[i + 1], __dmul_rn(lm, w.y));
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < B; ++i)
+                                if (i == ls) r[i] = 0.0;
+                        }
+                    }
+                } else {
+                    if (me == went) {
+#pragma unroll
+                        for (int i2 = 0; i2 < B / 2; ++i2) {
+                            const double2 w = uv[i2];
+                            const int i = 2 * i2;
+                            if (i > ls && i < bw) r[i] = w.x;
+                            if (i + 1 > ls && i + 1 < bw) r[i + 1] = w.y;
+                        }
+                    } else if (mypos > s && big) {
+                        const double lm = rsel<B>(r, ls);
+#pragma unroll
+                        for (int i2 = 0; i2 < B / 2; ++i2) {
+                            const double2 w = uv[i2];
+                            const int i = 2 * i2;
+                            if (i > ls && i < bw) r[i] = __dsub_rn(r[i], __dmul_rn(w.x, lm));
+                            if (i + 1 > ls && i + 1 < bw)
+                                r[i + 1] = __dsub_rn(r[i + 1], __dmul_rn(w.y, lm));
+                        }
+                    }
+                }
+            }
+            LU_T(4);
+            if (ls + 1 < bw) {
+                unsigned long long a = 0ULL;
+                unsigned key = 0xFFFFFFFFu;
+                if (mine && mypos >= s + 1) {
+                    a = (unsigned long long)__double_as_longlong(fabs(rsel<B>(r, ls + 1)));
+                    key = ((unsigned)mypos << 10) | (unsigned)tid;
+                }
+                cta_argmax(a, key, (s + 1) & 1);
+                stage_and_push(s + 1, bw);
+            }
+            LU_T(1);
+        }
+        __syncthreads();  // PR / pw_ent complete
+
+        // write the panel back; the multipliers go to this thread's tile row
+        // (the registers are free for the trailing update's 16-column block)
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+            if (i < bw) {
+                if (mine) wt[(int64_t)(J + i) * ldt + me] = r[i];
+                mytile[i] = r[i];
+            }
+
+        const int x0 = J + bw, tw = k - x0;
+        if (tw > 0) {
+            const int twp = (tw + 15) & ~15;
+            for (int t = tid; t < bw * twp; t += blockDim.x) {
+                const int ls = t / twp, c = t % twp;
+                Ach[ls * AW + c] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + pw_ent[ls]) : 0.0;
+            }
+            __syncthreads();
+            for (int c = tid; c < tw; c += blockDim.x) {
+                for (int ls = 0; ls < bw; ++ls) {
+                    double v = Ach[ls * AW + c];
+                    const double *pr = PR + ls * B;
+                    if (MODE == MODE_ROW) {
+                        for (int l2 = 0; l2 < ls; ++l2)
+                            v = __dsub_rn(v, __dmul_rn(pr[l2], Ach[l2 * AW + c]));
+                    } else {
+                        for (int l2 = 0; l2 < ls; ++l2)
+                            v = __dsub_rn(v, __dmul_rn(Ach[l2 * AW + c], pr[l2]));
+                        const double pv = pr[ls];
+                        v = fabs(pv) > thresh ? v / pv : 0.0;
+                    }
+                    Ach[ls * AW + c] = v;
+                    if (rank == 0) p.piv[(int64_t)(J + ls) * k + x0 + c] = v;
+                }
+            }
+            __syncthreads();
+            if (mine && mypos >= x0) {  // pivots are frozen
+                double *g = wt + (int64_t)x0 * ldt + me;
+                for (int c0 = 0; c0 < tw; c0 += 16) {
+                    double v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = c0 + i < tw ? g[(int64_t)(c0 + i) * ldt] : 0.0;
+                    for (int ls = 0; ls < bw; ++ls) {
+                        const double l = mytile[ls];
+                        const double2 *ar = reinterpret_cast<const double2 *>(Ach + ls * AW + c0);
+#pragma unroll
+                        for (int i2 = 0; i2 < 8; ++i2) {
+                            const double2 av = ar[i2];  // zero-padded past tw
+                            if (MODE == MODE_ROW) {
+                                v[2 * i2] = __dsub_rn(v[2 * i2], __dmul_rn(l, av.x));
+                                v[2 * i2 + 1] = __dsub_rn(v[2 * i2 + 1], __dmul_rn(l, av.y));
+                            } else {
+                                v[2 * i2] = __dsub_rn(v[2 * i2], __dmul_rn(av.x, l));
+                                v[2 * i2 + 1] = __dsub_rn(v[2 * i2 + 1], __dmul_rn(av.y, l));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (c0 + i < tw) g[(int64_t)(c0 + i) * ldt] = v[i];
+                }
+            }
+            __syncthreads();
+        }
+        LU_T(5);
+    }
+    LU_TDUMP();
+
+    // ---- final assembly through shared-memory tiles ----
+    cl.sync();
+    if (mine) {
+        qarr[tid] = mypos;
+        p.perm[mypos] = me;
+    }
+    const int q = mypos;
+    const int pend = q < k ? min(k, (q / b) * b + b) : k;
+    for (int x0 = 0; x0 < k; x0 += kLuTile) {
+        const int cw = min(kLuTile, k - x0);
+        if (mine)
+            for (int c = 0; c < cw; ++c) {
+                const int x = x0 + c;
+                const double v =
+                    x < pend ? wt[(int64_t)x * ldt + me] : __ldcg(p.piv + (int64_t)q * k + x);
+                double o;
+                if (MODE == MODE_ROW) {
+                    o = q >= k ? v : (x < q ? v : (x == q ? 1.0 : 0.0));
+                    if (q < k && p.out_small) p.out_small[(int64_t)q * p.ld_small + x] = x >= q ? v : 0.0;
+                } else {
+                    o = (q >= k || x <= q) ? v : 0.0;
+                    if (q < k) p.out_small[(int64_t)x * p.ld_small + q] = x > q ? v : (x == q ? 1.0 : 0.0);
+                }
+                mytile[c] = o;
+            }
+        __syncthreads();
+        for (int t = tid; t < ne * kLuTile; t += blockDim.x) {
+            const int e = t / kLuTile, c = t % kLuTile;
+            if (c < cw)
+                p.out_main[(int64_t)qarr[e] * p.ld_main + x0 + c] = tile[(size_t)e * (kLuTile + 1) + c];
+        }
+        __syncthreads();
+    }
+    cl.sync();  // no CTA exits while a peer could still address its shared memory
+}
+
+template <int B>
+static size_t lu_cluster_reg_smem_bytes(int rpc, int CL, int k) {
+    const int b = k < B ? k : B;
+    const int AW = ((k > b ? k - b : 1) + 15) & ~15;
+    return sizeof(double) * ((size_t)3 * CL * B + ((CL + 1) & ~1) + (size_t)32 * B + (size_t)B * B +
+                             (size_t)B * AW + (size_t)rpc * (kLuTile + 1)) +
+           sizeof(Cand) * 3 * CL + sizeof(int) * ((size_t)B + rpc) + 16;
+}
+
+// One pivot step on a register-resident panel row with the step index LS a
+// compile-time constant: only columns > LS are touched (no per-element
+// predication on LS).  Returns the entity's next-column value (argmax input).
+template <int MODE, int B, int LS>
+__device__ __forceinline__ double step_regs(double (&r)[B], const double *__restrict__ um,
+                                            double pivv, bool big, bool active, bool pivot_ent,
+                                            int bw) {
+    if (MODE == MODE_ROW) {
+        if (active) {
+            if (big) {
+                const double lm = r[LS] / pivv;
+                r[LS] = lm;
+#pragma unroll
+                for (int i = LS + 1; i < B; ++i)
+                    if (i < bw) r[i] = __dsub_rn(r[i], __dmul_rn(lm, um[i]));
+            } else {
+                r[LS] = 0.0;
+            }
+        }
+    } else {
+        if (pivot_ent) {
+#pragma unroll
+            for (int i = LS + 1; i < B; ++i)
+                if (i < bw) r[i] = um[i];
+        } else if (active && big) {
+            const double lm = r[LS];
+#pragma unroll
+            for (int i = LS + 1; i < B; ++i)
+                if (i < bw) r[i] = __dsub_rn(r[i], __dmul_rn(um[i], lm));
+        }
+    }
+    return LS + 1 < B ? r[LS + 1 < B ? LS + 1 : 0] : 0.0;
+}
+
+#define SRLU_STEP_CASE(L)                                                                   \
+    case L:                                                                                 \
+        if constexpr (L < B) nxt = step_regs<MODE, B, L>(r, um, pivv, big, act, piv_ent, bw); \
+        break;
+
+// ---------------------------------------------------------------------------
+// Hybrid LU (default for M <= 16384): ONE cooperative launch of G CTAs in
+// clusters of 16 (G = every co-resident cluster).  Cluster 0 runs each
+// panel's pivot steps exactly as lu_cluster_reg_kernel (registers rows,
+// DSMEM st.async exchange); then, after a grid barrier, ALL G CTAs apply the
+// panel's deferred trailing update to their own entity ranges, and a second
+// grid barrier hands the updated columns back to cluster 0.  The latency-
+// bound pivot chain stays inside one cluster while the FP64 trailing work
+// (most of the flops) runs on every SM.  Same per-element operation order.
+struct LuHybridParams {
+    LuParams p;
+    double *wt;   // k x ldt attribute-major working copy
+    int64_t ldt;
+    int *gpos;    // [M] position of each entity (written by cluster 0 per panel)
+    double *gPR;  // [B][B] the panel's pivot rows (panel part)
+    int *gpw;     // [B] the panel's pivot entities
+    double *gpart;  // [G] partial sums of squares
+};
+
+template <int MODE, int B>
+__global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ unsigned long long s_wabs[2][32];
+    __shared__ unsigned s_wkey[2][32];
+    __shared__ unsigned long long s_babs[2];
+    __shared__ unsigned s_bkey[2];
+    __shared__ double s_wsum[32];
+    __shared__ double s_thresh;
+    __shared__ __align__(8) uint64_t xbar[3];
+    __shared__ __align__(16) double s_own[B];
+    __shared__ int s_pw[B];
+
+    const LuParams &p = hp.p;
+    double *const wt = hp.wt;
+    const int64_t ldt = hp.ldt;
+    cg::grid_group grid = cg::this_grid();
+    cg::cluster_group cl = cg::this_cluster();
+    const int G = gridDim.x, bid = blockIdx.x;
+    const bool panel_cta = bid < (int)cl.num_blocks();  // cluster 0
+    const int rank = (int)cl.block_rank();
+    const int CL = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int k = p.k;
+    const int64_t M = p.M;
+    const int b = k < B ? k : B;
+    const int AW = ((k > b ? k - b : 1) + 15) & ~15;
+    // phase-A ownership (cluster 0): entity rank*rpcA + tid
+    const int rpcA = (int)ceil_div(M, (int64_t)CL);
+    const int64_t eA0 = (int64_t)rank * rpcA;
+    const int neA = (int)max((int64_t)0, min((int64_t)rpcA, M - eA0));
+    const bool mineA = panel_cta && tid < neA;
+    const int64_t meA = eA0 + tid;
+    // whole-grid ownership (prologue, trailing, epilogue): [eT0, eT0 + neT)
+    const int rpcT = (int)ceil_div(M, (int64_t)G);
+    const int64_t eT0 = (int64_t)bid * rpcT;
+    const int neT = (int)max((int64_t)0, min((int64_t)rpcT, M - eT0));
+
+    double *xrow = reinterpret_cast<double *>(smem_raw);                 // [3][CL][B]
+    Cand *xcand = reinterpret_cast<Cand *>(xrow + (size_t)3 * CL * B);   // [3][CL]
+    double *ucol = reinterpret_cast<double *>(xcand + 3 * CL);           // [32][B]
+    double *PR = ucol + 32 * B;                                          // B x B
+    double *Ach = PR + B * B;                                            // B x AW
+    double *tile = Ach + (size_t)B * AW;                                 // rpcT x (kLuTile+1)
+    int *qarr = reinterpret_cast<int *>(tile + (size_t)rpcT * (kLuTile + 1));  // rpcT
+    int mypos = (int)meA;
+    double r[B];
+
+    auto cta_argmax = [&](unsigned long long a, unsigned key, int par) {
+        warp_argmax_redux(a, key);
+        if (lane == 0) { s_wabs[par][warp] = a; s_wkey[par][warp] = key; }
+        __syncthreads();
+        if (warp == 0) {
+            a = lane < nwarps ? s_wabs[par][lane] : 0ULL;
+            key = lane < nwarps ? s_wkey[par][lane] : 0xFFFFFFFFu;
+            warp_argmax_redux(a, key);
+            if (lane == 0) { s_babs[par] = a; s_bkey[par] = key; }
+        }
+        __syncthreads();
+    };
+    auto step_bytes = [&](int st) -> unsigned {
+        const int bw_s = min(b, k - (st / b) * b);
+        return (unsigned)(CL * (((bw_s + 1) >> 1) * 16 + 16));
+    };
+    auto stage_and_push = [&](int st, int bw_s) {
+        const int par = st & 1;
+        const unsigned long long babs = s_babs[par];
+        const unsigned bkey = s_bkey[par];
+        const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);
+        if (warp != (owner >= 0 ? owner >> 5 : 0)) return;
+        if (tid == owner) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) s_own[i] = r[i];
+        }
+        __syncwarp();
+        const int sl = st % 3;
+        const int npair = (bw_s + 1) >> 1;
+        const unsigned pos = owner >= 0 ? (bkey >> 10) : 0xFFFFFFFFu;
+        const int ent = owner >= 0 ? (int)(eA0 + owner) : -1;
+        const unsigned dst = (unsigned)(lane & 15);
+        if ((int)dst < CL) {
+            const unsigned rbar = mapa_rank(smem_u32(&xbar[sl]), dst);
+            const unsigned rrow = mapa_rank(smem_u32(xrow + ((size_t)sl * CL + rank) * B), dst);
+            const int half = (npair + 1) >> 1;
+            const int i0 = lane < 16 ? 0 : half, i1 = lane < 16 ? half : npair;
+            for (int it = i0; it < i1; ++it) {
+                const int x = 2 * it;
+                const double v0 = owner >= 0 ? s_own[x] : 0.0;
+                const double v1 = owner >= 0 && x + 1 < bw_s ? s_own[x + 1] : 0.0;
+                st_async_f64x2(rrow + 16u * (unsigned)it, v0, v1, rbar);
+            }
+            if (lane >= 16)
+                st_async_u64x2(mapa_rank(smem_u32(xcand + sl * CL + rank), dst), babs,
+                               ((unsigned long long)(unsigned)ent << 32) | pos, rbar);
+        }
+    };
+
+    if (panel_cta && tid == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init_cta(smem_u32(&xbar[i]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 3 && i < k; ++i) mbar_arrive_expect_tx_cta(smem_u32(&xbar[i]), step_bytes(i));
+    }
+    // ---- prologue (all CTAs): transpose own range into wt; positions;
+    // ||w||_F^2 partial per CTA ----
+    double ss = 0.0;
+    for (int x0 = 0; x0 < k; x0 += kLuTile) {
+        const int cw = min(kLuTile, k - x0);
+        for (int t = tid; t < neT * kLuTile; t += blockDim.x) {
+            const int e = t / kLuTile, c = t % kLuTile;
+            if (c < cw) tile[(size_t)e * (kLuTile + 1) + c] = p.w[(eT0 + e) * p.ld + x0 + c];
+        }
+        __syncthreads();
+        if (tid < neT)
+            for (int c = 0; c < cw; ++c) {
+                const double v = tile[(size_t)tid * (kLuTile + 1) + c];
+                wt[(int64_t)(x0 + c) * ldt + eT0 + tid] = v;
+                ss += v * v;
+            }
+        __syncthreads();
+    }
+    if (tid < neT) hp.gpos[eT0 + tid] = (int)(eT0 + tid);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) s_wsum[warp] = ss;
+    __syncthreads();
+    if (warp == 0) {
+        double v = lane < nwarps ? s_wsum[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) hp.gpart[bid] = v;
+    }
+    cl.sync();    // cluster 0: barriers initialised before any remote access
+    grid.sync();  // wt, gpos, partials complete
+    if (tid == 0) {
+        double tot = 0.0;
+        for (int c = 0; c < G; ++c) tot += __ldcg(hp.gpart + c);
+        s_thresh = kPivotRtol * sqrt(tot);
+    }
+    __syncthreads();
+    const double thresh = s_thresh;
+    LU_T0();
+
+    for (int J = 0; J < k; J += b) {
+        const int bw = min(b, k - J);
+        // ======== phase A: the panel's pivot steps (cluster 0) ========
+        if (panel_cta) {
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                r[i] = (mineA && i < bw) ? __ldcg(wt + (int64_t)(J + i) * ldt + meA) : 0.0;
+            {
+                unsigned long long a = 0ULL;
+                unsigned key = 0xFFFFFFFFu;
+                if (mineA && mypos >= J) {
+                    a = (unsigned long long)__double_as_longlong(fabs(r[0]));
+                    key = ((unsigned)mypos << 10) | (unsigned)tid;
+                }
+                cta_argmax(a, key, J & 1);
+                stage_and_push(J, bw);
+            }
+            for (int ls = 0; ls < bw; ++ls) {
+                const int s = J + ls;
+                const int sl = s % 3;
+                LU_T(6);
+                mbar_wait_cluster(smem_u32(&xbar[sl]), (unsigned)((s / 3) & 1));
+                if (tid == 0 && s + 3 < k) mbar_arrive_expect_tx_cta(smem_u32(&xbar[sl]), step_bytes(s + 3));
+                LU_T(4);
+                unsigned long long ga = 0ULL;
+                unsigned gkey = 0xFFFFFFFFu;
+                if (lane < CL) {
+                    const Cand c = xcand[sl * CL + lane];
+                    if (c.entity >= 0) { ga = c.absbits; gkey = (c.pos << 4) | (unsigned)lane; }
+                }
+                warp_argmax_redux(ga, gkey);
+                const int gc = (int)(gkey & 15u);
+                const int wpos = (int)(gkey >> 4);
+                const int went = xcand[sl * CL + gc].entity;
+                const double *u = xrow + ((size_t)sl * CL + gc) * B;
+                const double pivv = u[ls];
+                const bool big = fabs(pivv) > thresh;
+                if (tid == 0) s_pw[ls] = went;
+                if (b < k && tid < bw)
+                    PR[ls * B + tid] = (MODE == MODE_COL && tid > ls) ? (big ? u[tid] / pivv : 0.0)
+                                                                      : u[tid];
+                if (mineA) {
+                    if (mypos == s) mypos = wpos;
+                    if (meA == went) mypos = s;
+                }
+                const double *um = u;
+                if (MODE == MODE_COL) {
+                    double *uw = ucol + warp * B;
+                    if (lane > ls && lane < bw) uw[lane] = big ? u[lane] / pivv : 0.0;
+                    __syncwarp();
+                    um = uw;
+                }
+                double nxt = 0.0;
+                if (mineA) {
+                    const bool act = mypos > s, piv_ent = meA == went;
+                    switch (ls) {
+                        SRLU_STEP_CASE(0) SRLU_STEP_CASE(1) SRLU_STEP_CASE(2) SRLU_STEP_CASE(3)
+                        SRLU_STEP_CASE(4) SRLU_STEP_CASE(5) SRLU_STEP_CASE(6) SRLU_STEP_CASE(7)
+                        SRLU_STEP_CASE(8) SRLU_STEP_CASE(9) SRLU_STEP_CASE(10) SRLU_STEP_CASE(11)
+                        SRLU_STEP_CASE(12) SRLU_STEP_CASE(13) SRLU_STEP_CASE(14) SRLU_STEP_CASE(15)
+                        default: break;
+                    }
+                }
+                LU_T(5);
+                if (ls + 1 < bw) {
+                    unsigned long long a = 0ULL;
+                    unsigned key = 0xFFFFFFFFu;
+                    if (mineA && mypos >= s + 1) {
+                        a = (unsigned long long)__double_as_longlong(fabs(nxt));
+                        key = ((unsigned)mypos << 10) | (unsigned)tid;
+                    }
+                    cta_argmax(a, key, (s + 1) & 1);
+                    stage_and_push(s + 1, bw);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                if (mineA && i < bw) wt[(int64_t)(J + i) * ldt + meA] = r[i];
+            if (mineA) hp.gpos[meA] = mypos;
+            if (rank == 0) {
+                for (int t = tid; t < bw * B; t += blockDim.x) hp.gPR[t] = PR[t];
+                if (tid < bw) hp.gpw[tid] = s_pw[tid];
+            }
+        }
+        LU_T(0);
+        const int x0 = J + bw, tw = k - x0;
+        if (tw <= 0) break;
+        grid.sync();
+        LU_T(1);
+        // ======== phase C: the panel's trailing update (all CTAs) ========
+        {
+            const int twp = (tw + 15) & ~15;
+            for (int t = tid; t < bw * B; t += blockDim.x) PR[t] = __ldcg(hp.gPR + t);
+            if (tid < bw) s_pw[tid] = __ldcg(hp.gpw + tid);
+            __syncthreads();
+            for (int t = tid; t < bw * twp; t += blockDim.x) {
+                const int ls = t / twp, c = t % twp;
+                Ach[ls * AW + c] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + s_pw[ls]) : 0.0;
+            }
+            __syncthreads();
+            for (int c = tid; c < tw; c += blockDim.x) {
+                for (int ls = 0; ls < bw; ++ls) {
+                    double v = Ach[ls * AW + c];
+                    const double *pr = PR + ls * B;
+                    if (MODE == MODE_ROW) {
+                        for (int l2 = 0; l2 < ls; ++l2)
+                            v = __dsub_rn(v, __dmul_rn(pr[l2], Ach[l2 * AW + c]));
+                    } else {
+                        for (int l2 = 0; l2 < ls; ++l2)
+                            v = __dsub_rn(v, __dmul_rn(Ach[l2 * AW + c], pr[l2]));
+                        const double pv = pr[ls];
+                        v = fabs(pv) > thresh ? v / pv : 0.0;
+                    }
+                    Ach[ls * AW + c] = v;
+                    if (bid == 0) p.piv[(int64_t)(J + ls) * k + x0 + c] = v;
+                }
+            }
+            __syncthreads();
+            // (entity, column group) per thread: consecutive threads take
+            // consecutive entities of the same columns (coalesced in wt)
+            if (neT > 0) {
+                const int ngrp = max(1, (int)blockDim.x / neT);
+                const int el = tid % neT, grp = tid / neT;
+                const int64_t e = eT0 + el;
+                if (grp < ngrp && __ldcg(hp.gpos + e) >= x0) {  // pivots are frozen
+                    double l[B];
+#pragma unroll
+                    for (int ls = 0; ls < B; ++ls)
+                        l[ls] = ls < bw ? __ldcg(wt + (int64_t)(J + ls) * ldt + e) : 0.0;
+                    // columns 4*grp + {0..3} + 4*ngrp*it: four independent loads
+                    // in flight per thread
+                    for (int c0 = 4 * grp; c0 < tw; c0 += 4 * ngrp) {
+                        double v[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            v[i] = c0 + i < tw ? __ldcg(wt + (int64_t)(x0 + c0 + i) * ldt + e) : 0.0;
+#pragma unroll
+                        for (int ls = 0; ls < B; ++ls)
+                            if (ls < bw) {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const double av = Ach[ls * AW + c0 + i];  // zero past tw
+                                    v[i] = MODE == MODE_ROW ? __dsub_rn(v[i], __dmul_rn(l[ls], av))
+                                                            : __dsub_rn(v[i], __dmul_rn(av, l[ls]));
+                                }
+                            }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (c0 + i < tw) wt[(int64_t)(x0 + c0 + i) * ldt + e] = v[i];
+                    }
+                }
+            }
+        }
+        LU_T(2);
+        grid.sync();
+        LU_T(3);
+    }
+    LU_TDUMP();
+
+    // ---- final assembly (all CTAs) through shared-memory tiles ----
+    grid.sync();
+    const int q = tid < neT ? __ldcg(hp.gpos + eT0 + tid) : 0;
+    if (tid < neT) {
+        qarr[tid] = q;
+        p.perm[q] = eT0 + tid;
+    }
+    const int pend = q < k ? min(k, (q / b) * b + b) : k;
+    for (int x0 = 0; x0 < k; x0 += kLuTile) {
+        const int cw = min(kLuTile, k - x0);
+        if (tid < neT)
+            for (int c = 0; c < cw; ++c) {
+                const int x = x0 + c;
+                const double v = x < pend ? __ldcg(wt + (int64_t)x * ldt + eT0 + tid)
+                                          : __ldcg(p.piv + (int64_t)q * k + x);
+                double o;
+                if (MODE == MODE_ROW) {
+                    o = q >= k ? v : (x < q ? v : (x == q ? 1.0 : 0.0));
+                    if (q < k && p.out_small) p.out_small[(int64_t)q * p.ld_small + x] = x >= q ? v : 0.0;
+                } else {
+                    o = (q >= k || x <= q) ? v : 0.0;
+                    if (q < k) p.out_small[(int64_t)x * p.ld_small + q] = x > q ? v : (x == q ? 1.0 : 0.0);
+                }
+                tile[(size_t)tid * (kLuTile + 1) + c] = o;
+            }
+        __syncthreads();
+        for (int t = tid; t < neT * kLuTile; t += blockDim.x) {
+            const int e = t / kLuTile, c = t % kLuTile;
+            if (c < cw)
+                p.out_main[(int64_t)qarr[e] * p.ld_main + x0 + c] = tile[(size_t)e * (kLuTile + 1) + c];
+        }
+        __syncthreads();
+    }
+}
+
+template <int B>
+static size_t lu_hybrid_smem_bytes(int rpcT, int CL, int k) {
+    const int b = k < B ? k : B;
+    const int AW = ((k > b ? k - b : 1) + 15) & ~15;
+    return sizeof(double) * ((size_t)3 * CL * B + (size_t)32 * B + (size_t)B * B + (size_t)B * AW +
+                             (size_t)rpcT * (kLuTile + 1)) +
+           sizeof(Cand) * 3 * CL + sizeof(int) * (size_t)rpcT + 16;
 }
 
 // the cluster path is considered for M <= 16 * 1024 entities
@@ -803,61 +1624,182 @@ static int sm_count() {
 // Cluster path when the panels of all M entities fit one cluster's shared
 // memory with a useful panel width; returns SRLU_OK when launched, 1 when the
 // shape (or the device) does not qualify.
+template <typename Kern>
+static int launch_lu_cluster(Kern kern, int CL, size_t smem, LuClusterParams cp,
+                             cudaStream_t stream, bool *launched) {
+    *launched = false;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return SRLU_OK;
+    }
+    if (CL > 8 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        return SRLU_OK;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (void *)kern, &cfg) != cudaSuccess ||
+        nclusters < 1) {
+        cudaGetLastError();
+        return SRLU_OK;
+    }
+    SRLU_CUDA(cudaLaunchKernelEx(&cfg, kern, cp));
+    *launched = true;
+    return SRLU_OK;
+}
+
+template <int MODE, int B>
+static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool *launched) {
+    *launched = false;
+    const int64_t M = prm.M;
+    const int k = prm.k;
+    constexpr int CL = 16;
+    auto kern = lu_hybrid_kernel<MODE, B>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return SRLU_OK;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.blockDim = dim3(1024);
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    // grid = every co-resident cluster (smem depends on the per-CTA range)
+    int ncl = 0;
+    size_t smem = 0;
+    for (int guess = 9; guess >= 1; --guess) {
+        const int rpcT = (int)ceil_div(M, (int64_t)(guess * CL));
+        smem = lu_hybrid_smem_bytes<B>(rpcT, CL, k);
+        if (smem > 220 * 1024) return SRLU_OK;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return SRLU_OK;
+        }
+        cfg.gridDim = dim3(guess * CL);
+        cfg.dynamicSmemBytes = smem;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, (void *)kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return SRLU_OK;
+        }
+        if (n >= guess) { ncl = guess; break; }
+    }
+    if (ncl < 1 || ceil_div(M, (int64_t)CL) > 1024) return SRLU_OK;
+    const int G = ncl * CL;
+    LuHybridParams hp;
+    hp.p = prm;
+    hp.p.b = k < B ? k : B;
+    hp.p.bs = hp.p.b | 1;
+    hp.p.rpc = (int)ceil_div(M, (int64_t)CL);
+    hp.ldt = lu_cluster_ldt(M);
+    char *base = (char *)ws + ((lu_base_workspace(k) + 255) & ~(size_t)255);
+    hp.wt = (double *)base;
+    char *extra = base + sizeof(double) * (size_t)k * hp.ldt;
+    hp.gpos = (int *)extra;
+    extra += ((size_t)M * sizeof(int) + 255) & ~(size_t)255;
+    hp.gPR = (double *)extra;
+    extra += 256 * sizeof(double) + 256;
+    hp.gpart = (double *)extra;
+    extra += 256 * sizeof(double);
+    hp.gpw = (int *)extra;
+    (void)G;
+    SRLU_CUDA(cudaLaunchKernelEx(&cfg, kern, hp));
+    *launched = true;
+    return SRLU_OK;
+}
+
+template <int MODE>
+static int try_run_lu_hybrid(LuParams prm, void *ws, cudaStream_t stream) {
+    if (const char *env = getenv("SRLU_LU_NO_HYBRID"))  // testing knob
+        if (atoi(env)) return 1;
+    if (prm.M > kLuClusterMaxM || prm.k > 1024) return 1;
+    bool launched = false;
+    const int rc = prm.k <= 8 ? try_run_lu_hybrid_b<MODE, 8>(prm, ws, stream, &launched)
+                              : try_run_lu_hybrid_b<MODE, 12>(prm, ws, stream, &launched);
+    if (rc != SRLU_OK) return rc;
+    return launched ? SRLU_OK : 1;
+}
+
 template <int MODE>
 static int try_run_lu_cluster(LuParams prm, void *ws, cudaStream_t stream) {
     if (const char *env = getenv("SRLU_LU_NO_CLUSTER"))  // testing knob
         if (atoi(env)) return 1;
+    const bool v4 = getenv("SRLU_LU_CLUSTER_V4") != nullptr;  // shared-memory rows (comparison)
     const int64_t M = prm.M;
     const int k = prm.k;
     if (M > kLuClusterMaxM || k > 1024) return 1;
-    auto kern = lu_cluster_kernel<MODE>;
     const size_t budget = 220 * 1024;
+    LuClusterParams cp;
+    cp.p = prm;
+    cp.ldt = lu_cluster_ldt(M);
+    cp.wt = (double *)((char *)ws + ((lu_base_workspace(k) + 255) & ~(size_t)255));
     for (int CL : {16, 8}) {
         const int64_t rpc64 = ceil_div(M, (int64_t)CL);
         if (rpc64 > 1024) continue;  // one entity per thread
         const int rpc = (int)rpc64;
-        int b = k < 32 ? k : 32;  // slot rows / per-warp multipliers hold <= 32
-        while (b > 1 && lu_cluster_smem_bytes(rpc, b, b | 1, CL, k) > budget) --b;
-        if (b < (k < 8 ? k : 8) || lu_cluster_smem_bytes(rpc, b, b | 1, CL, k) > budget) continue;
-        const size_t smem = lu_cluster_smem_bytes(rpc, b, b | 1, CL, k);
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return 1;
-        }
-        if (CL > 8 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                cudaSuccess) {
-            cudaGetLastError();
-            continue;
-        }
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CL;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(CL);
-        cfg.blockDim = dim3(1024);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = stream;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, (void *)kern, &cfg) != cudaSuccess ||
-            nclusters < 1) {
-            cudaGetLastError();
-            continue;
-        }
-        LuClusterParams cp;
-        cp.p = prm;
-        cp.p.b = b;
-        cp.p.bs = b | 1;
         cp.p.rpc = rpc;
-        cp.ldt = lu_cluster_ldt(M);
-        cp.wt = (double *)((char *)ws + ((lu_base_workspace(k) + 255) & ~(size_t)255));
-        SRLU_CUDA(cudaLaunchKernelEx(&cfg, kern, cp));
-        return SRLU_OK;
+        bool launched = false;
+        if (!v4) {
+            // panel width B: 12 keeps the row plus the step's state within the
+            // 64 registers of a 1024-thread CTA (16 spills); 8 for tiny k
+            int B = k <= 8 ? 8 : 12;
+            if (const char *env = getenv("SRLU_LU_REG_B")) B = atoi(env);  // testing knob
+            size_t smem;
+            int rc;
+            if (B == 8) {
+                smem = lu_cluster_reg_smem_bytes<8>(rpc, CL, k);
+                if (smem > budget) continue;
+                cp.p.b = k < 8 ? k : 8;
+                cp.p.bs = cp.p.b | 1;
+                rc = launch_lu_cluster(lu_cluster_reg_kernel<MODE, 8>, CL, smem, cp, stream, &launched);
+            } else if (B == 16) {
+                smem = lu_cluster_reg_smem_bytes<16>(rpc, CL, k);
+                if (smem > budget) continue;
+                cp.p.b = k < 16 ? k : 16;
+                cp.p.bs = cp.p.b | 1;
+                rc = launch_lu_cluster(lu_cluster_reg_kernel<MODE, 16>, CL, smem, cp, stream, &launched);
+            } else {
+                smem = lu_cluster_reg_smem_bytes<12>(rpc, CL, k);
+                if (smem > budget) continue;
+                cp.p.b = k < 12 ? k : 12;
+                cp.p.bs = cp.p.b | 1;
+                rc = launch_lu_cluster(lu_cluster_reg_kernel<MODE, 12>, CL, smem, cp, stream, &launched);
+            }
+            if (rc != SRLU_OK) return rc;
+        } else {
+            int b = k < 32 ? k : 32;
+            while (b > 1 && lu_cluster_smem_bytes(rpc, b, b | 1, CL, k) > budget) --b;
+            if (b < (k < 8 ? k : 8) || lu_cluster_smem_bytes(rpc, b, b | 1, CL, k) > budget) continue;
+            cp.p.b = b;
+            cp.p.bs = b | 1;
+            const int rc = launch_lu_cluster(lu_cluster_kernel<MODE>, CL,
+                                             lu_cluster_smem_bytes(rpc, b, b | 1, CL, k), cp, stream,
+                                             &launched);
+            if (rc != SRLU_OK) return rc;
+        }
+        if (launched) return SRLU_OK;
     }
     return 1;
 }
@@ -883,8 +1825,10 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     prm.candrow = (double *)((char *)prm.cand + sizeof(Cand) * 2 * kLuMaxGrid);
     prm.piv = prm.candrow + (size_t)2 * kLuMaxGrid * k;
 
-    const int rc = try_run_lu_cluster<MODE>(prm, ws, stream);
+    int rc = try_run_lu_hybrid<MODE>(prm, ws, stream);
     if (rc <= 0) return rc;  // launched (0) or failed (<0)
+    rc = try_run_lu_cluster<MODE>(prm, ws, stream);
+    if (rc <= 0) return rc;
 
     int G = sm_count() - reserve_sms;
     if (G < 1) G = 1;
@@ -921,10 +1865,18 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
 
 using namespace srlu;
 
+// hybrid-path arrays after the attribute-major copy: gpos[M], gPR[16x16],
+// gpw[16], gpart[256]
+static size_t lu_hybrid_extra(int64_t M) {
+    return (((size_t)M * sizeof(int) + 255) & ~(size_t)255) + 256 * sizeof(double) + 256 +
+           256 * sizeof(double) + 256;
+}
+
 extern "C" size_t srlu_lu_workspace(int64_t M, int64_t k) {
     size_t n = lu_base_workspace(k);
-    if (M <= kLuClusterMaxM && k <= 1024)  // attribute-major copy for the cluster path
-        n = ((n + 255) & ~(size_t)255) + sizeof(double) * (size_t)k * lu_cluster_ldt(M);
+    if (M <= kLuClusterMaxM && k <= 1024)  // attribute-major copy for the cluster paths
+        n = ((n + 255) & ~(size_t)255) + sizeof(double) * (size_t)k * lu_cluster_ldt(M) +
+            lu_hybrid_extra(M);
     return n;
 }
 
