@@ -64,6 +64,20 @@ int srlu_seed_key(uint64_t seed, uint64_t key[2]);
 int srlu_draw_fast_transform(uint64_t seed, int64_t k, int64_t l, double *phase,
                              int64_t *sample_idx, int64_t *pad);
 
+/* build_composite(k, l, n, seed) (sketch.py:269-278) in ONE call: the
+ * transform stage (seed + 2**32) drawn on the host into `staging` (pinned,
+ * srlu_build_composite_staging bytes; the caller must not reuse it before the
+ * uploads on `stream` completed) and uploaded to phase[l] / sample_idx[k]
+ * (int32); the sparse stage drawn on the device (row_of[n], sign[n]) and its
+ * accumulation plan (sorted[n], bucket_ptr[l+1]) as srlu_sem_plan.
+ * *pad (host) = the transform's power-of-two length. */
+size_t srlu_build_composite_workspace(int64_t n, int64_t l);
+size_t srlu_build_composite_staging(int64_t k, int64_t l);
+int srlu_build_composite(uint64_t seed, int64_t k, int64_t l, int64_t n, int32_t *row_of,
+                         double *sign, int32_t *sorted, int32_t *bucket_ptr, double *phase,
+                         int32_t *sample_idx, int64_t *pad, void *staging, size_t staging_bytes,
+                         void *ws, size_t ws_bytes, srlu_stream_t stream);
+
 /* build_sem(l, n, seed) on the DEVICE: row_of[n] in [0,l), sign[n] = +-1.
  * Bit-exact with numpy Generator(Philox(seed)).integers (Lemire). */
 size_t srlu_draw_sem_workspace(int64_t n, int64_t l);

@@ -38,6 +38,9 @@ SIGNATURES = {
     "srlu_seed_key": (INT, [U64, P]),
     "srlu_draw_fast_transform": (INT, [U64, I64, I64, P, P, P]),
     "srlu_draw_sem_workspace": (SZ, [I64, I64]),
+    "srlu_build_composite_workspace": (SZ, [I64, I64]),
+    "srlu_build_composite_staging": (SZ, [I64, I64]),
+    "srlu_build_composite": (INT, [U64, I64, I64, I64, P, P, P, P, P, P, P, P, SZ, P, SZ, P]),
     "srlu_draw_sem": (INT, [U64, I64, I64, P, P, P, SZ, P]),
     "srlu_sem_plan_workspace": (SZ, [I64, I64]),
     "srlu_sem_plan": (INT, [P, P, I64, I64, P, P, P, SZ, P]),
@@ -103,7 +106,7 @@ def lib():
 class _LaunchCounter:
     """Number of libsrlu kernels enqueued (bench.py's ``gpu_launches``)."""
 
-    PER_CALL = {"build_sem": 3, "sem_plan": 4, "sketch_right_dense": 1, "sketch_right_csr": 1,
+    PER_CALL = {"build_sem": 3, "sem_plan": 4, "build_composite": 7, "sketch_right_dense": 1, "sketch_right_csr": 1,
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 4,
                 "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1,

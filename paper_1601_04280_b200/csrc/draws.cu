@@ -248,3 +248,48 @@ extern "C" int srlu_draw_sem(uint64_t seed, int64_t l, int64_t n, int32_t *row_o
     SRLU_CHECK_LAUNCH("draw_sem_kernel");
     return SRLU_OK;
 }
+
+// ---------------------------------------------------------------------------
+// build_composite (sketch.py:269-278) in one call: the transform stage's
+// draws on the host (sequential Fisher-Yates, as numpy) into the caller's
+// pinned staging buffer and uploaded on `stream`, then the sparse stage's
+// device draws and its accumulation plan — one host entry instead of the
+// dozen allocations / copies / launches of the separate calls.
+
+static size_t align256(size_t n) { return (n + 255) & ~(size_t)255; }
+
+extern "C" size_t srlu_build_composite_workspace(int64_t n, int64_t l) {
+    return align256(srlu_draw_sem_workspace(n, l)) + align256(srlu_sem_plan_workspace(n, l));
+}
+
+extern "C" size_t srlu_build_composite_staging(int64_t k, int64_t l) {
+    return sizeof(double) * (size_t)l + sizeof(int64_t) * (size_t)k + sizeof(int32_t) * (size_t)k + 64;
+}
+
+extern "C" int srlu_build_composite(uint64_t seed, int64_t k, int64_t l, int64_t n, int32_t *row_of,
+                                    double *sign, int32_t *sorted, int32_t *bucket_ptr,
+                                    double *phase, int32_t *sample_idx, int64_t *pad,
+                                    void *staging, size_t staging_bytes, void *ws, size_t ws_bytes,
+                                    srlu_stream_t stream) {
+    SRLU_REQUIRE(staging_bytes >= srlu_build_composite_staging(k, l), SRLU_ERR_WORKSPACE,
+                 "build_composite: staging too small");
+    SRLU_REQUIRE(ws_bytes >= srlu_build_composite_workspace(n, l), SRLU_ERR_WORKSPACE,
+                 "build_composite: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    double *ph = (double *)staging;
+    int64_t *idx64 = (int64_t *)(ph + l);
+    int32_t *idx32 = (int32_t *)(idx64 + k);
+    // transform stage: seed + 2**32 (sketch.py:36, :276)
+    int rc = srlu_draw_fast_transform(seed + (1ULL << 32), k, l, ph, idx64, pad);
+    if (rc != SRLU_OK) return rc;
+    for (int64_t i = 0; i < k; ++i) idx32[i] = (int32_t)idx64[i];
+    SRLU_CUDA(cudaMemcpyAsync(phase, ph, sizeof(double) * (size_t)l, cudaMemcpyHostToDevice, s));
+    SRLU_CUDA(cudaMemcpyAsync(sample_idx, idx32, sizeof(int32_t) * (size_t)k,
+                              cudaMemcpyHostToDevice, s));
+    char *w = (char *)ws;
+    const size_t ws_sem = align256(srlu_draw_sem_workspace(n, l));
+    rc = srlu_draw_sem(seed, l, n, row_of, sign, w, ws_sem, stream);
+    if (rc != SRLU_OK) return rc;
+    return srlu_sem_plan(row_of, sign, n, l, sorted, bucket_ptr, w + ws_sem, ws_bytes - ws_sem,
+                         stream);
+}

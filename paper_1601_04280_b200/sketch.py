@@ -11,6 +11,7 @@ Walsh-Hadamard field is on the B200 path (every BASELINE config is real).
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field as dc_field
 
@@ -179,10 +180,81 @@ class CompositeSketch:
         return (self.out_dim, self.in_dim)
 
 
-def build_composite(k, l, n, kind, seed, device=None) -> CompositeSketch:
-    """sketch.py:269-278 (transform stage seeded seed + 2**32)."""
-    return CompositeSketch(build_sem(l, n, seed, device),
-                           build_fast_transform(k, l, kind, seed + STAGE_SEED_OFFSET, device))
+class _StagingPool:
+    """Pinned host staging buffers for the transform-stage draws, reused
+    once the upload that last read them has completed (event-guarded)."""
+
+    def __init__(self):
+        self._free = []  # (nbytes, pinned uint8 tensor, event)
+
+    def get(self, nbytes):
+        for i, (nb, buf, ev) in enumerate(self._free):
+            if nb >= nbytes and ev.query():
+                del self._free[i]
+                return buf
+        return torch.empty(max(nbytes, 4096), dtype=torch.uint8, pin_memory=True)
+
+    def put(self, buf, stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self._free.append((buf.numel(), buf, ev))
+        if len(self._free) > 8:
+            self._free.pop(0)
+
+
+_STAGING = _StagingPool()
+
+
+def build_composite(k, l, n, kind, seed, device=None, stream=None) -> CompositeSketch:
+    """sketch.py:269-278 (transform stage seeded seed + 2**32), in one C-ABI
+    call: host transform draws -> pinned staging -> upload, device sparse
+    draws and the accumulation plan, all enqueued on `stream`."""
+    if kind not in (FOURIER, HADAMARD):
+        raise ParameterError(f"unknown transform kind {kind!r}")
+    if kind == FOURIER:
+        raise NotImplementedError("the complex128 / FFT lane is out of scope of the B200 path")
+    if not 1 <= l <= n:
+        raise ParameterError(f"need 1 <= k <= n, got k={l}, n={n}")
+    pad = _next_pow2(l)
+    if not 1 <= k <= pad:
+        raise ParameterError(f"need 1 <= k <= {pad}, got k={k}")
+    seed = _check_seed(seed)
+    L = _lib.lib()
+    dev = torch.device(device) if device is not None else _default_device()
+    # one device allocation carved into the sketch's arrays (8-byte arrays first)
+    n8, l8 = n * 8, l * 8
+    i4 = lambda c: ((c * 4 + 7) // 8) * 8
+    off_sign, off_phase = 0, n8
+    off_row = off_phase + l8
+    off_sorted = off_row + i4(n)
+    off_bptr = off_sorted + i4(n)
+    off_idx = off_bptr + i4(l + 1)
+    off_ws = ((off_idx + i4(k)) + 255) // 256 * 256
+    ws_bytes = L.srlu_build_composite_workspace(n, l)
+    buf = torch.empty(off_ws + ws_bytes, dtype=torch.uint8, device=dev)
+    isz = {torch.float64: 8, torch.int32: 4}
+    view = lambda off, cnt, dt: buf[off:off + cnt * isz[dt]].view(dt)
+    sign = view(off_sign, n, torch.float64)
+    phase = view(off_phase, l, torch.float64)
+    row_of = view(off_row, n, torch.int32)
+    srt = view(off_sorted, n, torch.int32)
+    bptr = view(off_bptr, l + 1, torch.int32)
+    idx = view(off_idx, k, torch.int32)
+    st_bytes = L.srlu_build_composite_staging(k, l)
+    staging = _STAGING.get(st_bytes)
+    padc = ctypes.c_int64(0)
+    sh = _lib.stream_handle(stream)
+    _lib.check(L.srlu_build_composite(seed, k, l, n, _lib.ptr(row_of), _lib.ptr(sign),
+                                      _lib.ptr(srt), _lib.ptr(bptr), _lib.ptr(phase), _lib.ptr(idx),
+                                      ctypes.addressof(padc), staging.data_ptr(), staging.numel(),
+                                      buf.data_ptr() + off_ws, ws_bytes, sh), "build_composite")
+    _STAGING.put(staging, stream if stream is not None else torch.cuda.current_stream(dev))
+    assert padc.value == pad
+    sem = SparseEmbedding(int(l), int(n), row_of, sign, seed=seed)
+    sem._plan.extend([srt, bptr])
+    fast = FastTransformSketch(int(k), int(l), phase, idx, pad, math.sqrt(pad / k), kind,
+                               seed=seed + STAGE_SEED_OFFSET)
+    return CompositeSketch(sem, fast)
 
 
 # ---------------------------------------------------------------------------
