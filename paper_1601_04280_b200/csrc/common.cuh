@@ -98,6 +98,23 @@ __device__ inline void grid_arrive_wait(unsigned int *counter, unsigned int targ
 
 __device__ inline double ld_cg(const double *p) { return __ldcg(p); }
 
+// a / b correctly rounded (bit-identical to the IEEE division) from the
+// correctly rounded reciprocal y = __drcp_rn(b), shared by many dividends:
+// q0 = RN(a y), r = a - b q0 exact (FMA), q = RN(q0 + r y) (Markstein's
+// correction).  Outside the range where the theorem's no-underflow /
+// no-overflow conditions hold (and for zeros, inf, NaN) it takes the real
+// division.  Checked bit for bit against a / b on 1e10 random, hard-rounding
+// and edge-case pairs (tools/check_div.cu).
+__device__ __forceinline__ double div_by_recip(double a, double b, double y) {
+    const double fb = fabs(b), fa = fabs(a);
+    if (!(fb >= 0x1p-1000 && fb <= 0x1p+1000 && fa >= 0x1p-960 && fa <= 0x1p+1000)) return a / b;
+    const double q0 = __dmul_rn(a, y);
+    const double fq = fabs(q0);
+    if (!(fq >= 0x1p-960 && fq <= 0x1p+1000)) return a / b;
+    const double r = __fma_rn(-b, q0, a);
+    return __fma_rn(r, y, q0);
+}
+
 template <typename T> struct ValueTraits;
 template <> struct ValueTraits<float> { static constexpr int code = SRLU_F32; };
 template <> struct ValueTraits<double> { static constexpr int code = SRLU_F64; };

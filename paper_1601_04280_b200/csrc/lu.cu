@@ -1232,7 +1232,7 @@ __device__ __forceinline__ double step_regs(double (&r)[B], const double *__rest
 
 #define SRLU_STEP_CASE(L)                                                                   \
     case L:                                                                                 \
-        if constexpr (L < B) nxt = step_regs<MODE, B, L>(r, um, pivv, big, act, piv_ent, bw); \
+        if constexpr (L < B) nxt = step_regs<MODE, B, L>(rj, um, pivv, big, act, piv_ent, bw); \
         break;
 
 // ---------------------------------------------------------------------------
@@ -1254,8 +1254,9 @@ struct LuHybridParams {
     double *gpart;  // [G] partial sums of squares
 };
 
-template <int MODE, int B>
-__global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
+template <int MODE, int B, int RPT>
+__global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams hp) {
+    constexpr int NT = 1024 / RPT;  // RPT entities per thread in the panel phase
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_wabs[2][32];
     __shared__ unsigned s_wkey[2][32];
@@ -1282,12 +1283,19 @@ __global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
     const int64_t M = p.M;
     const int b = k < B ? k : B;
     const int AW = ((k > b ? k - b : 1) + 15) & ~15;
-    // phase-A ownership (cluster 0): entity rank*rpcA + tid
+    // phase-A ownership (cluster 0): local entities tid + j*NT, j < RPT
     const int rpcA = (int)ceil_div(M, (int64_t)CL);
     const int64_t eA0 = (int64_t)rank * rpcA;
     const int neA = (int)max((int64_t)0, min((int64_t)rpcA, M - eA0));
-    const bool mineA = panel_cta && tid < neA;
-    const int64_t meA = eA0 + tid;
+    bool mineA[RPT];
+    int64_t meA[RPT];
+    int mypos[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        mineA[j] = panel_cta && tid + j * NT < neA;
+        meA[j] = eA0 + tid + j * NT;
+        mypos[j] = (int)meA[j];
+    }
     // whole-grid ownership (prologue, trailing, epilogue): [eT0, eT0 + neT)
     const int rpcT = (int)ceil_div(M, (int64_t)G);
     const int64_t eT0 = (int64_t)bid * rpcT;
@@ -1300,8 +1308,7 @@ __global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
     double *Ach = PR + B * B;                                            // B x AW
     double *tile = Ach + (size_t)B * AW;                                 // rpcT x (kLuTile+1)
     int *qarr = reinterpret_cast<int *>(tile + (size_t)rpcT * (kLuTile + 1));  // rpcT
-    int mypos = (int)meA;
-    double r[B];
+    double r[RPT][B];
 
     auto cta_argmax = [&](unsigned long long a, unsigned key, int par) {
         warp_argmax_redux(a, key);
@@ -1323,11 +1330,17 @@ __global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
         const int par = st & 1;
         const unsigned long long babs = s_babs[par];
         const unsigned bkey = s_bkey[par];
-        const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);
-        if (warp != (owner >= 0 ? owner >> 5 : 0)) return;
-        if (tid == owner) {
+        const int owner = bkey == 0xFFFFFFFFu ? -1 : (int)(bkey & 1023u);  // local entity
+        const int othr = owner >= 0 ? owner % NT : 0;
+        if (warp != (othr >> 5)) return;
+        if (owner >= 0 && tid == othr) {
+            const int oj = owner / NT;
 #pragma unroll
-            for (int i = 0; i < B; ++i) s_own[i] = r[i];
+            for (int j = 0; j < RPT; ++j)
+                if (j == oj) {
+#pragma unroll
+                    for (int i = 0; i < B; ++i) s_own[i] = r[j][i];
+                }
         }
         __syncwarp();
         const int sl = st % 3;
@@ -1402,15 +1415,21 @@ __global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
         // ======== phase A: the panel's pivot steps (cluster 0) ========
         if (panel_cta) {
 #pragma unroll
-            for (int i = 0; i < B; ++i)
-                r[i] = (mineA && i < bw) ? __ldcg(wt + (int64_t)(J + i) * ldt + meA) : 0.0;
+            for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+                    r[j][i] = (mineA[j] && i < bw) ? __ldcg(wt + (int64_t)(J + i) * ldt + meA[j]) : 0.0;
             {
                 unsigned long long a = 0ULL;
                 unsigned key = 0xFFFFFFFFu;
-                if (mineA && mypos >= J) {
-                    a = (unsigned long long)__double_as_longlong(fabs(r[0]));
-                    key = ((unsigned)mypos << 10) | (unsigned)tid;
-                }
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (mineA[j] && mypos[j] >= J) {
+                        const unsigned long long aj =
+                            (unsigned long long)__double_as_longlong(fabs(r[j][0]));
+                        const unsigned kj = ((unsigned)mypos[j] << 10) | (unsigned)(tid + j * NT);
+                        if (better(aj, kj, a, key)) { a = aj; key = kj; }
+                    }
                 cta_argmax(a, key, J & 1);
                 stage_and_push(J, bw);
             }
@@ -1438,10 +1457,12 @@ __global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
                 if (b < k && tid < bw)
                     PR[ls * B + tid] = (MODE == MODE_COL && tid > ls) ? (big ? u[tid] / pivv : 0.0)
                                                                       : u[tid];
-                if (mineA) {
-                    if (mypos == s) mypos = wpos;
-                    if (meA == went) mypos = s;
-                }
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (mineA[j]) {
+                        if (mypos[j] == s) mypos[j] = wpos;
+                        if (meA[j] == went) mypos[j] = s;
+                    }
                 const double *um = u;
                 if (MODE == MODE_COL) {
                     double *uw = ucol + warp * B;
@@ -1449,34 +1470,43 @@ __global__ void __launch_bounds__(1024, 1) lu_hybrid_kernel(LuHybridParams hp) {
                     __syncwarp();
                     um = uw;
                 }
-                double nxt = 0.0;
-                if (mineA) {
-                    const bool act = mypos > s, piv_ent = meA == went;
-                    switch (ls) {
-                        SRLU_STEP_CASE(0) SRLU_STEP_CASE(1) SRLU_STEP_CASE(2) SRLU_STEP_CASE(3)
-                        SRLU_STEP_CASE(4) SRLU_STEP_CASE(5) SRLU_STEP_CASE(6) SRLU_STEP_CASE(7)
-                        SRLU_STEP_CASE(8) SRLU_STEP_CASE(9) SRLU_STEP_CASE(10) SRLU_STEP_CASE(11)
-                        SRLU_STEP_CASE(12) SRLU_STEP_CASE(13) SRLU_STEP_CASE(14) SRLU_STEP_CASE(15)
-                        default: break;
+                unsigned long long ca = 0ULL;
+                unsigned ckey = 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    double nxt = 0.0;
+                    if (mineA[j]) {
+                        double (&rj)[B] = r[j];
+                        const bool act = mypos[j] > s, piv_ent = meA[j] == went;
+                        switch (ls) {
+                            SRLU_STEP_CASE(0) SRLU_STEP_CASE(1) SRLU_STEP_CASE(2) SRLU_STEP_CASE(3)
+                            SRLU_STEP_CASE(4) SRLU_STEP_CASE(5) SRLU_STEP_CASE(6) SRLU_STEP_CASE(7)
+                            SRLU_STEP_CASE(8) SRLU_STEP_CASE(9) SRLU_STEP_CASE(10) SRLU_STEP_CASE(11)
+                            SRLU_STEP_CASE(12) SRLU_STEP_CASE(13) SRLU_STEP_CASE(14) SRLU_STEP_CASE(15)
+                            default: break;
+                        }
+                        if (mypos[j] >= s + 1) {
+                            const unsigned long long aj =
+                                (unsigned long long)__double_as_longlong(fabs(nxt));
+                            const unsigned kj = ((unsigned)mypos[j] << 10) | (unsigned)(tid + j * NT);
+                            if (better(aj, kj, ca, ckey)) { ca = aj; ckey = kj; }
+                        }
                     }
                 }
                 LU_T(5);
                 if (ls + 1 < bw) {
-                    unsigned long long a = 0ULL;
-                    unsigned key = 0xFFFFFFFFu;
-                    if (mineA && mypos >= s + 1) {
-                        a = (unsigned long long)__double_as_longlong(fabs(nxt));
-                        key = ((unsigned)mypos << 10) | (unsigned)tid;
-                    }
-                    cta_argmax(a, key, (s + 1) & 1);
+                    cta_argmax(ca, ckey, (s + 1) & 1);
                     stage_and_push(s + 1, bw);
                 }
             }
             __syncthreads();
 #pragma unroll
-            for (int i = 0; i < B; ++i)
-                if (mineA && i < bw) wt[(int64_t)(J + i) * ldt + meA] = r[i];
-            if (mineA) hp.gpos[meA] = mypos;
+            for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+                    if (mineA[j] && i < bw) wt[(int64_t)(J + i) * ldt + meA[j]] = r[j][i];
+                if (mineA[j]) hp.gpos[meA[j]] = mypos[j];
+            }
             if (rank == 0) {
                 for (int t = tid; t < bw * B; t += blockDim.x) hp.gPR[t] = PR[t];
                 if (tid < bw) hp.gpw[tid] = s_pw[tid];
@@ -1662,13 +1692,13 @@ static int launch_lu_cluster(Kern kern, int CL, size_t smem, LuClusterParams cp,
     return SRLU_OK;
 }
 
-template <int MODE, int B>
+template <int MODE, int B, int RPT>
 static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool *launched) {
     *launched = false;
     const int64_t M = prm.M;
     const int k = prm.k;
     constexpr int CL = 16;
-    auto kern = lu_hybrid_kernel<MODE, B>;
+    auto kern = lu_hybrid_kernel<MODE, B, RPT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
         cudaGetLastError();
         return SRLU_OK;
@@ -1681,7 +1711,7 @@ static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeCooperative;
     attr[1].val.cooperative = 1;
-    cfg.blockDim = dim3(1024);
+    cfg.blockDim = dim3(1024 / RPT);
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
@@ -1706,7 +1736,9 @@ static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool
         }
         if (n >= guess) { ncl = guess; break; }
     }
-    if (ncl < 1 || ceil_div(M, (int64_t)CL) > 1024) return SRLU_OK;
+    if (ncl < 1 || ceil_div(M, (int64_t)CL) > 1024 ||
+        ceil_div(M, (int64_t)(ncl * CL)) > 1024 / RPT)  // one entity per thread outside phase A
+        return SRLU_OK;
     const int G = ncl * CL;
     LuHybridParams hp;
     hp.p = prm;
@@ -1736,8 +1768,8 @@ static int try_run_lu_hybrid(LuParams prm, void *ws, cudaStream_t stream) {
         if (atoi(env)) return 1;
     if (prm.M > kLuClusterMaxM || prm.k > 1024) return 1;
     bool launched = false;
-    const int rc = prm.k <= 8 ? try_run_lu_hybrid_b<MODE, 8>(prm, ws, stream, &launched)
-                              : try_run_lu_hybrid_b<MODE, 12>(prm, ws, stream, &launched);
+    const int rc = prm.k <= 8 ? try_run_lu_hybrid_b<MODE, 8, 2>(prm, ws, stream, &launched)
+                              : try_run_lu_hybrid_b<MODE, 12, 2>(prm, ws, stream, &launched);
     if (rc != SRLU_OK) return rc;
     return launched ? SRLU_OK : 1;
 }

@@ -37,7 +37,7 @@ int main(int argc, char **argv) {
         cudaEventElapsedTime(&ms, e0, e1);
         long long t[8];
         cudaMemcpyFromSymbol(t, g_lu_trace, sizeof(t));
-        printf("rc=%d %.1f us | phaseA %lld sync1 %lld phaseC %lld sync2 %lld wait %lld win+upd %lld argmax+push %lld"
+        printf("rc=%d %.1f us | winner %lld bookkeep %lld argmax+push %lld phases %lld wait %lld first %lld rest %lld"
                " (cycles, rank 0)  %s\n", rc, ms * 1e3, t[0], t[1], t[2], t[3], t[4], t[5], t[6],
                cudaGetErrorString(cudaGetLastError()));
     }

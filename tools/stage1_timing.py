@@ -18,7 +18,6 @@ for it in range(8):
     e[0].record()
     om1 = build_composite(params.k1, params.l1, A.shape[1], kind, params.seed, A.device)
     e[1].record()
-    om1.sem.plan()
     e[2].record()
     y = torch.empty(A.shape[0], params.k1, dtype=torch.float64, device="cuda")
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -27,23 +26,18 @@ for it in range(8):
     torch.cuda.synchronize()
     res.append([e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])])
 r = np.median(np.array(res[2:]), axis=0) * 1e3
-print("draws %.1f us  plan %.1f us  K1 (incl. y alloc) %.1f us" % tuple(r))
+print("build_composite %.1f us  - %.1f  K1 (incl. y alloc) %.1f us" % tuple(r))
 
-# host enqueue time of the pieces (no sync inside)
+# host enqueue time of the one-call build
 import time
-from paper_1601_04280_b200.sketch import build_sem, build_fast_transform
 hs = []
 for it in range(20):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sem = build_sem(params.l1, A.shape[1], params.seed, A.device)
+    om = build_composite(params.k1, params.l1, A.shape[1], kind, params.seed, A.device)
     t1 = time.perf_counter()
-    ft = build_fast_transform(params.k1, params.l1, kind, params.seed + 2**32, A.device)
-    t2 = time.perf_counter()
-    sem.plan()
-    t3 = time.perf_counter()
     torch.cuda.synchronize()
-    t4 = time.perf_counter()
-    hs.append([t1 - t0, t2 - t1, t3 - t2, t4 - t3])
+    t2 = time.perf_counter()
+    hs.append([t1 - t0, t2 - t1])
 h = np.median(np.array(hs[3:]), axis=0) * 1e6
-print("host us: build_sem %.1f  build_fast_transform %.1f  plan %.1f  then GPU drain %.1f" % tuple(h))
+print("host us: build_composite %.1f  then GPU drain %.1f" % tuple(h))
