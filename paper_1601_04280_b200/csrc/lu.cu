@@ -1235,6 +1235,60 @@ __device__ __forceinline__ double step_regs(double (&r)[B], const double *__rest
         if constexpr (L < B) nxt = step_regs<MODE, B, L>(rj, um, pivv, big, act, piv_ent, bw); \
         break;
 
+// The same step split at the critical path: step_first touches column LS+1
+// only (the next pivot column), step_rest columns LS+2.. afterwards, while
+// the exchange of the next step is in flight.
+template <int MODE, int B, int LS>
+__device__ __forceinline__ double step_first(double (&r)[B], const double *__restrict__ um,
+                                             double pivv, bool big, bool active, bool pivot_ent,
+                                             int bw, bool &upd) {
+    constexpr int N1 = LS + 1 < B ? LS + 1 : B - 1;
+    const bool has1 = LS + 1 < B && LS + 1 < bw;
+    if (MODE == MODE_ROW) {
+        if (active) {
+            if (big) {
+                const double lm = r[LS] / pivv;
+                r[LS] = lm;
+                if (has1) r[N1] = __dsub_rn(r[N1], __dmul_rn(lm, um[N1]));
+                upd = true;
+            } else {
+                r[LS] = 0.0;
+            }
+        }
+    } else {
+        if (pivot_ent) {
+#pragma unroll
+            for (int i = LS + 1; i < B; ++i)
+                if (i < bw) r[i] = um[i];
+        } else if (active && big) {
+            if (has1) r[N1] = __dsub_rn(r[N1], __dmul_rn(um[N1], r[LS]));
+            upd = true;
+        }
+    }
+    return has1 ? r[N1] : 0.0;
+}
+
+template <int MODE, int B, int LS>
+__device__ __forceinline__ void step_rest(double (&r)[B], const double *__restrict__ um, int bw) {
+    const double lm = r[LS];  // ROW: the multiplier; COL: the pivot-column value
+#pragma unroll
+    for (int i = LS + 2; i < B; ++i)
+        if (i < bw)
+            r[i] = MODE == MODE_ROW ? __dsub_rn(r[i], __dmul_rn(lm, um[i]))
+                                    : __dsub_rn(r[i], __dmul_rn(um[i], lm));
+}
+
+#define SRLU_CASES_16(M)                                                                  \
+    M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15)
+#define SRLU_FIRST_CASE(L)                                                                 \
+    case L:                                                                                \
+        if constexpr (L < B) nxt = step_first<MODE, B, L>(rj, um, pivv, big, act, piv_ent, bw, updj); \
+        break;
+#define SRLU_REST_CASE(L)                                                                  \
+    case L:                                                                                \
+        if constexpr (L < B) step_rest<MODE, B, L>(rj, um, bw);                            \
+        break;
+
 // ---------------------------------------------------------------------------
 // Hybrid LU (default for M <= 16384): ONE cooperative launch of G CTAs in
 // clusters of 16 (G = every co-resident cluster).  Cluster 0 runs each
@@ -1470,6 +1524,61 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
                     __syncwarp();
                     um = uw;
                 }
+                if constexpr (MODE == MODE_ROW) {  // critical-path split (row LU)
+                unsigned long long ca = 0ULL;
+                unsigned ckey = 0xFFFFFFFFu;
+                bool upd[RPT];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    double nxt = 0.0;
+                    bool updj = false;
+                    if (mineA[j]) {
+                        double (&rj)[B] = r[j];
+                        const bool act = mypos[j] > s, piv_ent = meA[j] == went;
+                        switch (ls) {
+                            SRLU_CASES_16(SRLU_FIRST_CASE)
+                            default: break;
+                        }
+                        if (mypos[j] >= s + 1) {
+                            const unsigned long long aj =
+                                (unsigned long long)__double_as_longlong(fabs(nxt));
+                            const unsigned kj = ((unsigned)mypos[j] << 10) | (unsigned)(tid + j * NT);
+                            if (better(aj, kj, ca, ckey)) { ca = aj; ckey = kj; }
+                        }
+                    }
+                    upd[j] = updj;
+                }
+                auto rest_row = [&](int j) {
+#pragma unroll
+                    for (int jj = 0; jj < RPT; ++jj)
+                        if (jj == j) {
+                            double (&rj)[B] = r[jj];
+                            switch (ls) {
+                                SRLU_CASES_16(SRLU_REST_CASE)
+                                default: break;
+                            }
+                        }
+                };
+                if (ls + 1 < bw) {
+                    cta_argmax(ca, ckey, (s + 1) & 1);
+                    // the owner completes its row before its warp stages it
+                    const unsigned bk = s_bkey[(s + 1) & 1];
+                    if (bk != 0xFFFFFFFFu && (int)(bk & 1023u) % NT == tid) {
+                        const int oj = (int)(bk & 1023u) / NT;
+#pragma unroll
+                        for (int j = 0; j < RPT; ++j)
+                            if (j == oj && upd[j]) {
+                                rest_row(j);
+                                upd[j] = false;
+                            }
+                    }
+                    stage_and_push(s + 1, bw);
+                }
+                // the rest of the rows, overlapping the exchange of step s+1
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (upd[j]) rest_row(j);
+                } else {  // one pass per step (column LU: the split measured slower)
                 unsigned long long ca = 0ULL;
                 unsigned ckey = 0xFFFFFFFFu;
 #pragma unroll
@@ -1479,10 +1588,7 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
                         double (&rj)[B] = r[j];
                         const bool act = mypos[j] > s, piv_ent = meA[j] == went;
                         switch (ls) {
-                            SRLU_STEP_CASE(0) SRLU_STEP_CASE(1) SRLU_STEP_CASE(2) SRLU_STEP_CASE(3)
-                            SRLU_STEP_CASE(4) SRLU_STEP_CASE(5) SRLU_STEP_CASE(6) SRLU_STEP_CASE(7)
-                            SRLU_STEP_CASE(8) SRLU_STEP_CASE(9) SRLU_STEP_CASE(10) SRLU_STEP_CASE(11)
-                            SRLU_STEP_CASE(12) SRLU_STEP_CASE(13) SRLU_STEP_CASE(14) SRLU_STEP_CASE(15)
+                            SRLU_CASES_16(SRLU_STEP_CASE)
                             default: break;
                         }
                         if (mypos[j] >= s + 1) {
@@ -1493,10 +1599,10 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
                         }
                     }
                 }
-                LU_T(5);
                 if (ls + 1 < bw) {
                     cta_argmax(ca, ckey, (s + 1) & 1);
                     stage_and_push(s + 1, bw);
+                }
                 }
             }
             __syncthreads();
