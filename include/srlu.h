@@ -105,6 +105,25 @@ int srlu_sketch_right_dense(const void *a, int dtype, int64_t m, int64_t n, int6
                             int64_t pad1, double mult1, double *y, int64_t ldy,
                             int *nonfinite, srlu_stream_t stream);
 
+/* Scheduled K1 (same result, bit for bit; replaces the same reference lines
+ * as srlu_sketch_right_dense).  srlu_k1_schedule_bytes returns 0 when the
+ * shape is outside the scheduled kernel's range (rows of more than four
+ * 32 KB chunks, l1 > 3584, pad1 outside [32, 8192]); the caller then uses
+ * srlu_sketch_right_dense.  srlu_k1_schedule builds, from the plan of
+ * srlu_sem_plan, the per-warp gather schedule (bank-conflict-free 16-bit
+ * codes) into `sched`; it depends only on the sketch, n and dtype and can
+ * be reused for every A with that shape.  A must be 16-byte aligned with a
+ * 16-byte row pitch. */
+size_t srlu_k1_schedule_bytes(int64_t n, int64_t l1, int64_t pad1, int dtype);
+int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bucket_ptr1, int64_t n, int64_t l1,
+                     int64_t pad1, int dtype, void *sched, size_t sched_bytes,
+                     srlu_stream_t stream);
+int srlu_sketch_right_dense_sched(const void *a, int dtype, int64_t m, int64_t n, int64_t lda,
+                                  const void *sched, size_t sched_bytes, int64_t l1,
+                                  const double *phase1, const int32_t *idx1, int64_t k1,
+                                  int64_t pad1, double mult1, double *y, int64_t ldy,
+                                  int *nonfinite, srlu_stream_t stream);
+
 /* A in CSR: indptr[m+1] (int64), indices (int32, ascending per row),
  * values (dtype).  row_of1/sign1: the raw draws. */
 int srlu_sketch_right_csr(const int64_t *indptr, const int32_t *indices, const void *vals,

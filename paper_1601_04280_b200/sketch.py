@@ -59,6 +59,7 @@ class SparseEmbedding:
     sign: torch.Tensor     # float64 [in_dim], +-1
     seed: int = 0
     _plan: list = dc_field(default_factory=list, repr=False)
+    _sched: list = dc_field(default_factory=list, repr=False)
 
     @property
     def shape(self):
@@ -78,6 +79,26 @@ class SparseEmbedding:
                        "sem_plan")
             self._plan.extend([srt, bptr])
         return self._plan[0], self._plan[1]
+
+    def k1_schedule(self, dtype_code, pad, stream=None):
+        """Gather schedule of the scheduled K1 kernel (srlu_k1_schedule) for
+        an A of this element type, built once per (dtype, pad) on `stream`;
+        None when the shape is outside that kernel's range."""
+        key = ("k1s", dtype_code, pad)
+        for k_, v in self._sched:
+            if k_ == key:
+                return v
+        L = _lib.lib()
+        nbytes = L.srlu_k1_schedule_bytes(self.in_dim, self.out_dim, pad, dtype_code)
+        buf = None
+        if nbytes:
+            srt, bptr = self.plan(stream)
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=srt.device)
+            _lib.check(L.srlu_k1_schedule(_lib.ptr(srt), _lib.ptr(bptr), self.in_dim, self.out_dim,
+                                          pad, dtype_code, _lib.ptr(buf), nbytes,
+                                          _lib.stream_handle(stream)), "k1_schedule")
+        self._sched.append((key, buf))
+        return buf
 
     def row_counts(self):
         return torch.bincount(self.row_of.long(), minlength=self.out_dim)
@@ -281,6 +302,17 @@ def sketch_right_into(a: Matrix, omega: CompositeSketch, y: torch.Tensor, nonfin
             y.stride(0), _lib.ptr(nonfinite), sh), "sketch_right_csr")
     else:
         t = a.raw
+        dcode = _lib.dtype_code(t.dtype)
+        es = t.element_size()
+        aligned = t.data_ptr() % 16 == 0 and (t.stride(0) * es) % 16 == 0 and (n * es) % 16 == 0
+        sched = sem.k1_schedule(dcode, fast.pad, stream) if aligned else None
+        if sched is not None:
+            _lib.check(L.srlu_sketch_right_dense_sched(
+                _lib.ptr(t), dcode, m, n, t.stride(0), _lib.ptr(sched), sched.numel(),
+                sem.out_dim, _lib.ptr(fast.phase), _lib.ptr(fast.sample_idx), fast.out_dim,
+                fast.pad, fast.mult, _lib.ptr(y), y.stride(0), _lib.ptr(nonfinite), sh),
+                "sketch_right_dense_sched")
+            return
         srt, bptr = sem.plan()
         _lib.check(L.srlu_sketch_right_dense(
             _lib.ptr(t), _lib.dtype_code(t.dtype), m, n, t.stride(0), _lib.ptr(srt),
