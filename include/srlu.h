@@ -115,6 +115,11 @@ int srlu_sketch_right_dense(const void *a, int dtype, int64_t m, int64_t n, int6
  * be reused for every A with that shape.  A must be 16-byte aligned with a
  * 16-byte row pitch. */
 size_t srlu_k1_schedule_bytes(int64_t n, int64_t l1, int64_t pad1, int dtype);
+/* the scheduled kernel's geometry for a shape (diagnostics): info = {rows
+ * per block, bucket slots per lane, chunk columns, chunks, stages, code
+ * bytes that fit in shared memory, shared memory bytes, max lanes per bank};
+ * SRLU_ERR_UNSUPPORTED (info zeroed) when the shape is not scheduled. */
+int srlu_k1_config(int64_t n, int64_t l1, int64_t pad1, int dtype, int64_t info[8]);
 int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bucket_ptr1, int64_t n, int64_t l1,
                      int64_t pad1, int dtype, void *sched, size_t sched_bytes,
                      srlu_stream_t stream);

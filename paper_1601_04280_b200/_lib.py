@@ -47,6 +47,7 @@ SIGNATURES = {
     "srlu_sketch_right_dense": (INT, [P, INT, I64, I64, I64, P, P, I64, P, P, I64, I64, DBL,
                                       P, I64, P, P]),
     "srlu_k1_schedule_bytes": (SZ, [I64, I64, I64, INT]),
+    "srlu_k1_config": (INT, [I64, I64, I64, INT, P]),
     "srlu_k1_schedule": (INT, [P, P, I64, I64, I64, INT, P, SZ, P]),
     "srlu_sketch_right_dense_sched": (INT, [P, INT, I64, I64, I64, P, SZ, I64, P, P, I64, I64,
                                             DBL, P, I64, P, P]),

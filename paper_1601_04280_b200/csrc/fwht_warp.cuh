@@ -66,6 +66,50 @@ __device__ __forceinline__ void fwht_block_warp(double *blk, int lane) {
     __syncwarp();
 }
 
+// Stages h = 1..16 of one value per lane (index j = 32*q + lane): the
+// reference's butterflies (a + b, a - b), lower index first, via shuffles.
+__device__ __forceinline__ double fwht_lane_stages(double v, int lane) {
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+        const double p = __shfl_xor_sync(0xffffffffu, v, h);
+        v = (lane & h) ? __dsub_rn(p, v) : __dadd_rn(v, p);
+    }
+    return v;
+}
+
+// The remaining stages h = 32 .. 16*E of a 32*E block whose stages h < 32
+// were already applied (fwht_lane_stages): layout B, registers only.
+template <int E>
+__device__ __forceinline__ void fwht_block_warp_hi(double *blk, int lane) {
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = blk[fwht_sw(e * 32 + lane)];
+#pragma unroll
+    for (int hh = 1; hh < E; hh <<= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & hh) == 0) {
+                const double a = v[e], b = v[e + hh];
+                v[e] = __dadd_rn(a, b);
+                v[e + hh] = __dsub_rn(a, b);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) blk[fwht_sw(e * 32 + lane)] = v[e];
+    __syncwarp();
+}
+
+__device__ __forceinline__ void fwht_block_warp_hi_dyn512(double *blk, int bsize, int lane) {
+    switch (bsize) {
+        case 512: fwht_block_warp_hi<16>(blk, lane); break;
+        case 256: fwht_block_warp_hi<8>(blk, lane); break;
+        case 128: fwht_block_warp_hi<4>(blk, lane); break;
+        case 64: fwht_block_warp_hi<2>(blk, lane); break;
+        default: break;  // 32: nothing left
+    }
+}
+
 // dispatch on the block length (32 <= pad <= 1024, power of two)
 __device__ __forceinline__ void fwht_block_warp_dyn(double *blk, int pad, int lane) {
     switch (pad) {
@@ -118,6 +162,26 @@ __device__ __forceinline__ double fwht_combine_blocks(const double *row, int bsi
     for (int b = 1; b < 16; ++b)
         if (b == B) r = u[b];
     return r;
+}
+
+// Output-pruned cross-block stages: the value at block B, in-block offset
+// o (swizzled) of the full transform whose NB blocks (stride bsize) were
+// transformed in place.  Only the NB-1 butterfly nodes feeding that output
+// are formed, level by level (stage h = bsize first), with exactly the
+// operands and order of the full network (bit-identical).
+template <int NB>
+__device__ __forceinline__ double wht_pick(const double *row, int bsize, int o, int B) {
+    double u[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) u[b] = row[b * bsize + o];
+#pragma unroll
+    for (int s = 1, lvl = 0; s < NB; s <<= 1, ++lvl) {
+        const bool neg = (B >> lvl) & 1;
+#pragma unroll
+        for (int i = 0; i < NB / (2 * s); ++i)
+            u[i] = neg ? __dsub_rn(u[2 * i], u[2 * i + 1]) : __dadd_rn(u[2 * i], u[2 * i + 1]);
+    }
+    return u[0];
 }
 
 }  // namespace srlu

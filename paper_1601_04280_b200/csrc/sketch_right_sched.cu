@@ -17,17 +17,22 @@
 // staged in shared memory when they fit.
 //
 // Kernel structure (persistent, one CTA per SM, 1024 threads):
-//   * a ring of kNS stages of RB rows x C columns, filled by 1-D bulk
-//     copies (cp.async.bulk + mbarrier); the last gather warp to release a
-//     stage refills it (no CTA-wide barrier in the stream);
-//   * 28 gather warps: fp64 register accumulators acc[BPT][RB], persisting
-//     across the chunks of a row block; then +-phase into a double-buffered
-//     FWHT scratch (mbarrier hand-off);
-//   * 4 epilogue warps: register FWHT per 512-point block, output-pruned
-//     cross-block stages, x mult, Y write, non-finite flag — overlapping the
-//     gathers of the next row block.
+//   * a ring of NS stages of RB rows x C columns, filled by 1-D bulk copies
+//     (cp.async.bulk + mbarrier); the last gather warp to release a stage
+//     refills it, so the stream never waits on a CTA-wide barrier;
+//   * 28 gather warps: fp64 register accumulators acc[BPT][RB] persisting
+//     across the chunks of a row block, then +-phase and the FWHT stages
+//     h < 32 by shuffles (lane = bucket bits 0..4) into a double-buffered
+//     scratch xs;
+//   * per row block, all 32 warps then run the stages 32 <= h < 512 (one
+//     thread per in-block column, registers) and the output-pruned stages
+//     h >= 512 for the k sampled outputs only (x mult, Y store, non-finite
+//     flag), between two CTA barriers — the bulk copies of the next stages
+//     stay in flight meanwhile.
 #include <limits.h>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "fwht_warp.cuh"
 #include "tma.cuh"
@@ -36,9 +41,8 @@ namespace srlu {
 
 namespace k1s {
 
-constexpr int kGW = 28;                 // gather warps
-constexpr int kEW = 4;                  // epilogue warps
-constexpr int kNT = (kGW + kEW) * 32;   // 1024 threads
+constexpr int kGW = 28;                 // gather warps (of 32)
+constexpr int kNT = 1024;
 constexpr int kMaxChunks = 4;
 constexpr int kMaxStages = 8;
 constexpr int kZeroBytes = 128;         // zero tail per staged row: one word per bank
@@ -46,10 +50,10 @@ constexpr size_t kSmemMax = 232448 - 1024;
 constexpr int kHeader = 16;             // int32 header words
 
 struct Cfg {
-    int es, rb, bpt, c, nch, ns, ng, zpad;
+    int es, rb, bpt, c, nch, ns, ng, zpad, d2;
     int64_t stage_bytes, row_stride, xs_bytes, code_cap, smem;
     // workspace offsets (bytes)
-    int64_t off_grp, off_np, off_sched, off_codes, ws_bytes;
+    int64_t off_grp, off_np, off_wsched, off_codes, ws_bytes;
 };
 
 static int env_int(const char *name, int dflt) {
@@ -67,9 +71,12 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
         if ((int64_t)kGW * b >= groups) { bpt = b; break; }
     if (!bpt) return false;
     const int64_t row_bytes = n * es;
-    int rb = env_int("SRLU_K1_RB", row_bytes <= 8192 ? 4 : (row_bytes <= 16384 ? 2 : 1));
+    // measured on B200 (tools/k1_sweep.py): two rows per block from 16 KB
+    // rows up, stages of one row but at least 32 KB and at most 64 KB
+    int rb = env_int("SRLU_K1_RB", row_bytes <= 8192 ? 4 : 2);
     if (rb != 1 && rb != 2 && rb != 4) return false;
-    const int64_t stage_target = env_int("SRLU_K1_STAGE", 32768);
+    const int64_t stage_target =
+        env_int("SRLU_K1_STAGE", (int)std::min<int64_t>(65536, std::max<int64_t>(32768, row_bytes)));
     int64_t cmax = stage_target / (rb * es);
     cmax &= ~31LL;
     if (cmax < 32) return false;
@@ -80,29 +87,36 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     Cfg f{};
     f.es = es; f.rb = rb; f.bpt = bpt; f.c = (int)c; f.nch = (int)nch;
     f.ng = kGW * bpt; f.zpad = kZeroBytes / es;
+    f.d2 = env_int("SRLU_K1_D", 2) >= 2 ? 2 : 1;
     f.row_stride = (c + f.zpad) * es;
     f.stage_bytes = rb * f.row_stride;
     f.xs_bytes = 2LL * rb * pad * 8;
+    // leave room for the codes (~64 B per warp step, ~n/16 steps)
+    const int64_t code_est = 4 * n + 4096;
     int ns = env_int("SRLU_K1_NS", 4);
     if (ns < 2) ns = 2;
     if (ns > kMaxStages) ns = kMaxStages;
-    while (ns > 2 && (size_t)(ns * f.stage_bytes + f.xs_bytes + 16384) > kSmemMax) --ns;
+    while (ns > 2 && (size_t)(ns * f.stage_bytes + f.xs_bytes + code_est) > kSmemMax) --ns;
     f.ns = ns;
     int64_t used = ns * f.stage_bytes + f.xs_bytes;
-    if ((size_t)used + 4096 > kSmemMax) return false;
+    if ((size_t)used > kSmemMax) return false;
     f.code_cap = ((int64_t)kSmemMax - used) & ~15LL;
     f.smem = used + f.code_cap;
-    // workspace: header | grp_bucket[ng*32] | np[nch*ng] | sched[nch*ng*2] | codes
+    // workspace: header | grp[ng*32] | np[nch*ng] | wsched[nch*kGW*2] | codes
     auto al = [](int64_t v) { return (v + 15) & ~15LL; };
     f.off_grp = al(kHeader * 4);
     f.off_np = al(f.off_grp + (int64_t)f.ng * 32 * 4);
-    f.off_sched = al(f.off_np + (int64_t)nch * f.ng * 4);
-    f.off_codes = al(f.off_sched + (int64_t)nch * f.ng * 8);
-    // every step advances >= 1 source; + one odd-padding step per (chunk, group)
-    f.ws_bytes = f.off_codes + 64 * (n + 2 * nch * (int64_t)f.ng) + 64;
+    f.off_wsched = al(f.off_np + (int64_t)nch * f.ng * 4);
+    f.off_codes = al(f.off_wsched + (int64_t)nch * kGW * 8);
+    // a step advances >= 1 source of its group; pairs round up; slots of a
+    // warp are padded to the longest: <= bpt * 16 * (n + 2 nch ng) words
+    f.ws_bytes = f.off_codes + 64LL * bpt * (n + 2 * nch * (int64_t)f.ng) + 64;
     *cf = f;
     return true;
 }
+
+// warp w, slot b -> group (snake order over the slots)
+__host__ __device__ inline int group_of(int w, int b) { return b * kGW + ((b & 1) ? kGW - 1 - w : w); }
 
 // ---------------------------------------------------------------------------
 // schedule construction
@@ -113,44 +127,66 @@ __global__ void group_kernel(int l, int ng, int32_t *grp) {
         grp[s] = s < l ? s : -1;
 }
 
-// One warp per group simulates the walk of its 32 lanes chunk by chunk.
-// PASS 0 counts steps (np = step pairs per (chunk, group)); PASS 1 recomputes
-// the layout offsets (chunk-major, then group) and writes the codes.
+// One warp per group simulates the walk of its 32 lanes chunk by chunk: in
+// each step every pending lane proposes its next source; per bank (per
+// half-warp bank pair for 8-byte elements) the D lanes with the longest
+// remaining queue win, the others read a zero word in a bank nobody uses.
+// PASS 0 counts step pairs per (chunk, group).  PASS 1 pads the slots of each
+// warp to a common pair count per chunk and writes the codes at
+// [chunk][warp][pair][slot][lane] (u32 = two 16-bit codes).
 template <int PASS>
 __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ sorted,
                                                    const int32_t *__restrict__ bptr, int c,
-                                                   int nch, int es8, int ng,
+                                                   int nch, int es8, int bpt, int d2,
                                                    const int32_t *__restrict__ grp,
-                                                   int32_t *np_tab, int32_t *sched,
+                                                   int32_t *np_tab, int32_t *wsched,
                                                    uint32_t *codes, int32_t *header) {
-    __shared__ unsigned best[32];
+    __shared__ unsigned best[32], best2[32];
     const int g = blockIdx.x, lane = threadIdx.x;
+    const int ng = kGW * bpt;
+    const int b = g / kGW, w = (b & 1) ? kGW - 1 - (g % kGW) : (g % kGW);
     const unsigned FULL = 0xffffffffu;
     const int t = grp[g * 32 + lane];
     int cur = t >= 0 ? bptr[t] : 0;
     const int end = t >= 0 ? bptr[t + 1] : 0;
     int nxt = cur < end ? sorted[cur] : INT_MAX;
     best[lane] = 0;
+    best2[lane] = 0;
     __syncwarp();
+    auto joint = [&](int ch, int ww) {  // pairs of warp ww in chunk ch
+        int mx = 0;
+        for (int bb = 0; bb < bpt; ++bb) mx = max(mx, np_tab[ch * ng + group_of(ww, bb)]);
+        return mx;
+    };
     for (int ch = 0; ch < nch; ++ch) {
         const int c0 = ch * c, c1 = c0 + c;
-        const int idx = ch * ng + g;
         uint32_t *out = nullptr;
+        int npj = 0;
         if (PASS == 1) {
+            // base of (ch, w): all (ch', w') before it in [chunk][warp] order
+            const int idx = ch * kGW + w;
             int s = 0;
-            for (int i = lane; i < idx; i += 32) s += np_tab[i];
+            for (int i = lane; i < idx; i += 32) s += joint(i / kGW, i % kGW);
 #pragma unroll
             for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-            const int base = s * 32;
-            if (lane == 0) {
-                sched[2 * idx] = base;
-                sched[2 * idx + 1] = np_tab[idx];
-                if (idx == nch * ng - 1) header[0] = base + np_tab[idx] * 32;
+            npj = joint(ch, w);
+            const int base = s * bpt * 32;
+            if (lane == 0 && b == 0) {
+                wsched[2 * idx] = base;
+                wsched[2 * idx + 1] = npj;
+                if (idx == nch * kGW - 1) header[0] = base + npj * bpt * 32;
             }
-            out = codes + base;
+            out = codes + base + b * 32 + lane;
         }
         int step = 0;
         uint32_t pairw = 0;
+        auto emit = [&](uint32_t code) {
+            if (PASS == 1) {
+                if (step & 1) out[(size_t)(step >> 1) * bpt * 32] = pairw | (code << 16);
+                else pairw = code;
+            }
+            ++step;
+        };
         while (true) {
             const int col = nxt & 0x7fffffff;
             const bool pend = nxt != INT_MAX && col < c1;
@@ -161,9 +197,17 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
             const unsigned prio = ((unsigned)min(rem, 1 << 20) << 5) | (unsigned)(31 - lane);
             if (pend) atomicMax(&best[key], prio);
             __syncwarp();
-            const bool win = pend && best[key] == prio;
+            bool win = pend && best[key] == prio;
+            if (d2 >= 2) {
+                if (pend && !win) atomicMax(&best2[key], prio);
+                __syncwarp();
+                win = win || (pend && best2[key] == prio);
+            }
             __syncwarp();
-            if (pend) best[key] = 0;
+            if (pend) {
+                best[key] = 0;
+                best2[key] = 0;
+            }
             const unsigned used = __reduce_or_sync(FULL, win ? (1u << key) : 0u);
             uint32_t code;
             if (win) {
@@ -174,22 +218,18 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
                 const int fk = __ffs((int)freem) - 1;  // exists: this lane did not win
                 code = (uint32_t)(c + fk);             // a zero word in that bank
             }
-            if (PASS == 1) {
-                if (step & 1) out[(step >> 1) * 32 + lane] = pairw | (code << 16);
-                else pairw = code;
-            }
+            emit(code);
             if (win) {
                 ++cur;
                 nxt = cur < end ? __ldg(sorted + cur) : INT_MAX;
             }
             __syncwarp();
-            ++step;
         }
-        if (step & 1) {  // pad the pair with a broadcast no-op (same zero word for all lanes)
-            if (PASS == 1) out[(step >> 1) * 32 + lane] = pairw | ((uint32_t)c << 16);
-            ++step;
-        }
-        if (PASS == 0 && lane == 0) np_tab[idx] = step >> 1;
+        // pad to the warp's common pair count with broadcast no-ops (every
+        // lane reads the same zero word)
+        const int target = PASS == 1 ? 2 * npj : step + (step & 1);
+        while (step < target) emit((uint32_t)c);
+        if (PASS == 0 && lane == 0) np_tab[ch * ng + g] = step >> 1;
     }
 }
 
@@ -197,7 +237,7 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
 // the sketch kernel
 
 struct Dev {
-    int c, nch, ns, ng;
+    int c, nch, ns, ng, dbg;
     int row_stride, stage_bytes;
     int xs_off, code_off, code_cap;
 };
@@ -224,10 +264,86 @@ __device__ __forceinline__ void gather_step(const unsigned char *st, int row_str
     }
 }
 
+// One gather warp's stream: per row block, per chunk, the warp's joint
+// schedule (all BPT slots step together); then +-phase, the FWHT stages
+// h < 32 by shuffles (slot g*32 + lane holds bucket g*32 + lane, zero if
+// empty) and the hand-off of the block to the epilogue warps.
+template <typename T, int RB, int BPT, typename Codes, typename Issue>
+__device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
+                                            const int32_t *__restrict__ grp,
+                                            const int2 *__restrict__ wsched,
+                                            const double *__restrict__ phase, const Dev &d,
+                                            int64_t my_nrb, int64_t nitems, uint64_t *full,
+                                            uint64_t *xs_full, uint64_t *xs_empty, unsigned *rel,
+                                            double *xs_base, int pad, const Issue &issue) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int gid[BPT];
+    bool bneg[BPT];
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        gid[b] = group_of(warp, b);
+        const int t = grp[gid[b] * 32 + lane];
+        bneg[b] = t >= 0 && phase[t] < 0.0;
+    }
+    int stage = 0;
+    unsigned ph = 0;
+    int64_t it = 0;
+    for (int64_t rbi = 0; rbi < my_nrb; ++rbi) {
+        double acc[BPT][RB];
+#pragma unroll
+        for (int b = 0; b < BPT; ++b)
+#pragma unroll
+            for (int r = 0; r < RB; ++r) acc[b][r] = 0.0;
+        for (int ch = 0; ch < d.nch; ++ch, ++it) {
+            const int2 sc = __ldg(wsched + ch * kGW + warp);
+            if (!(d.dbg & 8)) mbar_wait(&full[stage], ph);
+            const unsigned char *st = smem + stage * d.stage_bytes;
+            const int np = sc.y;
+            const int base = sc.x + lane;
+#pragma unroll(BPT == 1 ? 4 : (BPT == 2 ? 2 : 1))
+            for (int s2 = 0; s2 < np; ++s2) {
+#pragma unroll
+                for (int b = 0; b < BPT; ++b) {
+                    const uint32_t w = cw[base + (s2 * BPT + b) * 32];
+                    gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
+                    gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
+                }
+            }
+            // release the stage; the last of the kGW warps refills it
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                const unsigned old = atomicAdd(&rel[stage], 1u);
+                if ((old + 1) % kGW == 0 && it + d.ns < nitems && !(d.dbg & 8)) {
+                    fence_proxy_async_smem();
+                    issue(it + d.ns, stage);
+                }
+            }
+            if (++stage == d.ns) {
+                stage = 0;
+                ph ^= 1u;
+            }
+        }
+        const int buf = (int)(rbi & 1);
+        if (rbi >= 2) mbar_wait_sleep(&xs_empty[buf], (unsigned)(((rbi >> 1) - 1) & 1), 256);
+        double *xs = xs_base + (size_t)buf * RB * pad;
+#pragma unroll
+        for (int b = 0; b < BPT; ++b) {
+            const int pos = fwht_sw(gid[b] * 32 + lane);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const double v = fwht_lane_stages(bneg[b] ? -acc[b][r] : acc[b][r], lane);
+                if (gid[b] * 32 < pad) xs[r * pad + pos] = v;
+            }
+        }
+        mbar_arrive(&xs_full[buf]);
+    }
+}
+
 template <typename T, int RB, int BPT>
 __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
     const T *__restrict__ a, int64_t m, int64_t n, int64_t lda, const unsigned char *__restrict__ ws,
-    int64_t off_grp, int64_t off_sched, int64_t off_codes, int l, const double *__restrict__ phase,
+    int64_t off_grp, int64_t off_wsched, int64_t off_codes, int l, const double *__restrict__ phase,
     const int32_t *__restrict__ idx, int k, int pad, double mult, double *__restrict__ y,
     int64_t ldy, int *nonfinite, Dev d) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -240,18 +356,18 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
     const int64_t my_nrb = (int64_t)blockIdx.x < nrb ? ceil_div(nrb - blockIdx.x, gridDim.x) : 0;
     const int64_t nitems = my_nrb * d.nch;
     const int32_t *grp = reinterpret_cast<const int32_t *>(ws + off_grp);
-    const int2 *sched = reinterpret_cast<const int2 *>(ws + off_sched);
+    const int2 *wsched = reinterpret_cast<const int2 *>(ws + off_wsched);
     const uint32_t *codes_g = reinterpret_cast<const uint32_t *>(ws + off_codes);
     const int total_words = reinterpret_cast<const int32_t *>(ws)[0];
     double *xs_base = reinterpret_cast<double *>(smem + d.xs_off);
     uint32_t *codes_s = reinterpret_cast<uint32_t *>(smem + d.code_off);
-    const bool codes_in_smem = (int64_t)total_words * 4 <= d.code_cap;
+    const bool codes_in_smem = (int64_t)total_words * 4 <= d.code_cap && !(d.dbg & 4);
 
     if (tid == 0) {
         for (int s = 0; s < d.ns; ++s) mbar_init(&full[s], 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&xs_full[b], kGW * 32);
-            mbar_init(&xs_empty[b], kEW * 32);
+            mbar_init(&xs_empty[b], (kNT / 32 - kGW) * 32);
         }
         fence_mbar_init();
     }
@@ -272,119 +388,87 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
         for (int i = tid; i < nv; i += kNT) dst[i] = __ldg(src + i);
     }
     __syncthreads();
-    const uint32_t *cw = codes_in_smem ? codes_s : codes_g;
 
-    auto issue = [&](int64_t it) {
-        const int stage = (int)(it % d.ns);
-        const int64_t rbi = it / d.nch;
-        const int ch = (int)(it % d.nch);
-        const int64_t row0 = ((int64_t)blockIdx.x + rbi * gridDim.x) * RB;
+    uint64_t *fullp = full;
+    const int nch = d.nch, cc = d.c, sbytes = d.stage_bytes, rstride = d.row_stride;
+    const int64_t bid = blockIdx.x, gdim = gridDim.x;
+    auto issue = [=](int64_t it, int stage) {
+        const int64_t rbi = it / nch;
+        const int ch = (int)(it - rbi * nch);
+        const int64_t row0 = (bid + rbi * gdim) * RB;
         const int nrows = (int)min((int64_t)RB, m - row0);
-        const int64_t c0 = (int64_t)ch * d.c;
-        const int cols = (int)min((int64_t)d.c, n - c0);
+        const int64_t c0 = (int64_t)ch * cc;
+        const int cols = (int)min((int64_t)cc, n - c0);
         const unsigned bytes = (unsigned)cols * es;
-        unsigned char *st = smem + (size_t)stage * d.stage_bytes;
-        mbar_arrive_expect_tx(&full[stage], bytes * nrows);
+        unsigned char *st = smem + (size_t)stage * sbytes;
+        mbar_arrive_expect_tx(&fullp[stage], bytes * nrows);
         for (int r = 0; r < nrows; ++r)
-            bulk_g2s(st + (size_t)r * d.row_stride, a + (row0 + r) * lda + c0, bytes, &full[stage]);
+            bulk_g2s(st + (size_t)r * rstride, a + (row0 + r) * lda + c0, bytes, &fullp[stage]);
     };
-    if (tid == 0)
-        for (int64_t it = 0; it < d.ns && it < nitems; ++it) issue(it);
+    if (tid == 0 && !(d.dbg & 16))
+        for (int64_t it = 0; it < d.ns && it < nitems; ++it) issue(it, (int)it);
 
     if (warp < kGW) {
-        // ------------------------------------------------------------ gather
-        int bt[BPT], gid[BPT];
-        bool bneg[BPT];
-#pragma unroll
-        for (int b = 0; b < BPT; ++b) {
-            const int g = b * kGW + ((b & 1) ? kGW - 1 - warp : warp);
-            gid[b] = g;
-            bt[b] = grp[g * 32 + lane];
-            bneg[b] = bt[b] >= 0 && phase[bt[b]] < 0.0;
-        }
-        for (int64_t rbi = 0; rbi < my_nrb; ++rbi) {
-            double acc[BPT][RB];
-#pragma unroll
-            for (int b = 0; b < BPT; ++b)
-#pragma unroll
-                for (int r = 0; r < RB; ++r) acc[b][r] = 0.0;
-            for (int ch = 0; ch < d.nch; ++ch) {
-                const int64_t it = rbi * d.nch + ch;
-                const int stage = (int)(it % d.ns);
-                mbar_wait(&full[stage], (unsigned)((it / d.ns) & 1));
-                const unsigned char *st = smem + (size_t)stage * d.stage_bytes;
-#pragma unroll
-                for (int b = 0; b < BPT; ++b) {
-                    const int2 sc = __ldg(sched + ch * d.ng + gid[b]);
-                    const uint32_t *cp = cw + sc.x + lane;
-                    const int np = sc.y;
-#pragma unroll 4
-                    for (int s2 = 0; s2 < np; ++s2) {
-                        const uint32_t w = cp[s2 * 32];
-                        gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
-                        gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
-                    }
-                }
-                // release the stage; the last of the kGW warps refills it
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    const unsigned old = atomicAdd(&rel[stage], 1u);
-                    if ((old + 1) % kGW == 0 && it + d.ns < nitems) {
-                        fence_proxy_async_smem();
-                        issue(it + d.ns);
-                    }
-                }
-            }
-            const int buf = (int)(rbi & 1);
-            if (rbi >= 2) mbar_wait(&xs_empty[buf], (unsigned)(((rbi >> 1) - 1) & 1));
-            double *xs = xs_base + (size_t)buf * RB * pad;
-#pragma unroll
-            for (int b = 0; b < BPT; ++b) {
-                if (bt[b] >= 0) {
-                    const int pos = fwht_sw(bt[b]);
-#pragma unroll
-                    for (int r = 0; r < RB; ++r) xs[r * pad + pos] = bneg[b] ? -acc[b][r] : acc[b][r];
-                }
-            }
-            mbar_arrive(&xs_full[buf]);
-        }
-    } else {
-        // ---------------------------------------------------------- epilogue
-        const int ew = warp - kGW, etid = tid - kGW * 32;
-        const int bsize = pad < 512 ? pad : 512;
-        const int nb = pad / bsize;
-        const int nzb = (l + bsize - 1) / bsize;
-        bool bad = false;
-        for (int64_t rbi = 0; rbi < my_nrb; ++rbi) {
-            const int buf = (int)(rbi & 1);
-            mbar_wait(&xs_full[buf], (unsigned)((rbi >> 1) & 1));
-            double *xs = xs_base + (size_t)buf * RB * pad;
-            for (int item = ew; item < RB * nzb; item += kEW) {
-                const int r = item / nzb, bb = item % nzb;
-                fwht_block_warp_dyn512(xs + (size_t)r * pad + (size_t)bb * bsize, bsize, lane);
-            }
-            named_bar(1, kEW * 32);
-            const int64_t row0 = ((int64_t)blockIdx.x + rbi * gridDim.x) * RB;
-            const int nrows = (int)min((int64_t)RB, m - row0);
-            for (int w = etid; w < nrows * k; w += kEW * 32) {
-                const int r = w / k, kk = w % k;
-                const double v =
-                    __dmul_rn(fwht_combine_blocks(xs + (size_t)r * pad, bsize, nb, idx[kk]), mult);
-                y[(row0 + r) * ldy + kk] = v;
-                bad |= !isfinite(v);
-            }
-            named_bar(1, kEW * 32);
-            // the transformed blocks hold nonzeros at t >= l: re-zero them
-            const int tz = nzb * bsize;
-            for (int i = etid; i < RB * (tz - l); i += kEW * 32) {
-                const int r = i / (tz - l), t = l + i % (tz - l);
-                xs[(size_t)r * pad + fwht_sw(t)] = 0.0;
-            }
-            mbar_arrive(&xs_empty[buf]);
-        }
-        if (bad) atomicOr(nonfinite, 1);
+        if (codes_in_smem)
+            gather_warp<T, RB, BPT>(smem, codes_s, grp, wsched, phase, d, my_nrb, nitems, full,
+                                    xs_full, xs_empty, rel, xs_base, pad, issue);
+        else
+            gather_warp<T, RB, BPT>(smem, codes_g, grp, wsched, phase, d, my_nrb, nitems, full,
+                                    xs_full, xs_empty, rel, xs_base, pad, issue);
+        return;
     }
+    // ---------------------------------------------------------------- epilogue
+    constexpr int kEW = kNT / 32 - kGW;
+    const int ew = warp - kGW, etid = tid - kGW * 32;
+    const int bsize = pad < 512 ? pad : 512;
+    const int nb = pad / bsize;
+    const int nzb = (l + bsize - 1) / bsize;
+    bool bad = false;
+    for (int64_t rbi = 0; rbi < my_nrb; ++rbi) {
+        const int buf = (int)(rbi & 1);
+        mbar_wait_sleep(&xs_full[buf], (unsigned)((rbi >> 1) & 1), 32);
+        double *xs = xs_base + (size_t)buf * RB * pad;
+        // stages 32 <= h < bsize (the gather warps applied h < 32)
+        for (int item = ew; !(d.dbg & 1) && item < RB * nzb; item += kEW) {
+            const int r = item / nzb, bb = item % nzb;
+            fwht_block_warp_hi_dyn512(xs + (size_t)r * pad + (size_t)bb * bsize, bsize, lane);
+        }
+        named_bar(1, kEW * 32);
+        // output-pruned stages h >= bsize for the k sampled outputs only
+        const int64_t row0 = ((int64_t)blockIdx.x + rbi * gridDim.x) * RB;
+        const int nrows = (int)min((int64_t)RB, m - row0);
+        for (int kk = etid; !(d.dbg & 2) && kk < k; kk += kEW * 32) {
+            const int q = idx[kk];
+            const int o = fwht_sw(q & (bsize - 1)), B = q / bsize;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                if (r < nrows) {
+                    const double *row = xs + (size_t)r * pad;
+                    double f;
+                    switch (nb) {
+                        case 1: f = row[o]; break;
+                        case 2: f = wht_pick<2>(row, bsize, o, B); break;
+                        case 4: f = wht_pick<4>(row, bsize, o, B); break;
+                        case 8: f = wht_pick<8>(row, bsize, o, B); break;
+                        default: f = wht_pick<16>(row, bsize, o, B); break;
+                    }
+                    const double v = __dmul_rn(f, mult);
+                    y[(row0 + r) * ldy + kk] = v;
+                    bad |= !isfinite(v);
+                }
+            }
+        }
+        named_bar(1, kEW * 32);
+        // positions in [ng*32, nzb*bsize) are not rewritten by the gather
+        // warps but were transformed in place: re-zero them
+        const int z0 = d.ng * 32, z1 = nzb * bsize;
+        for (int i = etid; z1 > z0 && i < RB * (z1 - z0); i += kEW * 32) {
+            const int r = i / (z1 - z0), t = z0 + i % (z1 - z0);
+            xs[(size_t)r * pad + fwht_sw(t)] = 0.0;
+        }
+        mbar_arrive(&xs_empty[buf]);
+    }
+    if (bad) atomicOr(nonfinite, 1);
 }
 
 template <typename T, int RB, int BPT>
@@ -394,6 +478,7 @@ static int launch(const Cfg &f, const T *a, int64_t m, int64_t n, int64_t lda,
                   cudaStream_t s) {
     Dev d;
     d.c = f.c; d.nch = f.nch; d.ns = f.ns; d.ng = f.ng;
+    d.dbg = env_int("SRLU_K1_DBG", 0);  // experiments: 1 no FWHT, 2 no outputs, 8 no waits
     d.row_stride = (int)f.row_stride; d.stage_bytes = (int)f.stage_bytes;
     d.xs_off = (int)(f.ns * f.stage_bytes);
     d.code_off = (int)(d.xs_off + f.xs_bytes);
@@ -405,9 +490,9 @@ static int launch(const Cfg &f, const T *a, int64_t m, int64_t n, int64_t lda,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nrb = ceil_div(m, RB);
     const unsigned grid = (unsigned)(nrb < sms ? nrb : sms);
-    kern<<<grid, kNT, (size_t)f.smem, s>>>(a, m, n, lda, ws, f.off_grp, f.off_sched, f.off_codes,
-                                           (int)l, phase, idx, (int)k, (int)pad, mult, y, ldy,
-                                           nonfinite, d);
+    kern<<<grid, kNT, (size_t)f.smem, s>>>(a, m, n, lda, ws, f.off_grp, f.off_wsched,
+                                           f.off_codes, (int)l, phase, idx, (int)k, (int)pad,
+                                           mult, y, ldy, nonfinite, d);
     SRLU_CHECK_LAUNCH("k1s_kernel");
     return SRLU_OK;
 }
@@ -443,6 +528,19 @@ extern "C" size_t srlu_k1_schedule_bytes(int64_t n, int64_t l1, int64_t pad1, in
     return (size_t)f.ws_bytes;
 }
 
+extern "C" int srlu_k1_config(int64_t n, int64_t l1, int64_t pad1, int dtype, int64_t info[8]) {
+    const int es = es_of(dtype);
+    k1s::Cfg f;
+    SRLU_REQUIRE(info != nullptr, SRLU_ERR_ARG, "k1_config: null info");
+    if (!es || !k1s::config(n, l1, pad1, es, &f)) {
+        for (int i = 0; i < 8; ++i) info[i] = 0;
+        return SRLU_ERR_UNSUPPORTED;
+    }
+    info[0] = f.rb; info[1] = f.bpt; info[2] = f.c; info[3] = f.nch;
+    info[4] = f.ns; info[5] = f.code_cap; info[6] = f.smem; info[7] = f.d2;
+    return SRLU_OK;
+}
+
 extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, int64_t n,
                                 int64_t l1, int64_t pad1, int dtype, void *sched,
                                 size_t sched_bytes, srlu_stream_t stream) {
@@ -457,16 +555,16 @@ extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, in
     int32_t *header = (int32_t *)ws;
     int32_t *grp = (int32_t *)(ws + f.off_grp);
     int32_t *np = (int32_t *)(ws + f.off_np);
-    int32_t *sc = (int32_t *)(ws + f.off_sched);
+    int32_t *wsc = (int32_t *)(ws + f.off_wsched);
     uint32_t *codes = (uint32_t *)(ws + f.off_codes);
     k1s::group_kernel<<<(unsigned)ceil_div((int64_t)f.ng * 32, 256), 256, 0, s>>>((int)l1, f.ng,
                                                                                  grp);
     SRLU_CHECK_LAUNCH("k1s_group_kernel");
-    k1s::sched_kernel<0><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.ng, grp, np,
-                                             sc, codes, header);
+    k1s::sched_kernel<0><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.bpt, f.d2,
+                                             grp, np, wsc, codes, header);
     SRLU_CHECK_LAUNCH("k1s_sched_kernel<0>");
-    k1s::sched_kernel<1><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.ng, grp, np,
-                                             sc, codes, header);
+    k1s::sched_kernel<1><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.bpt, f.d2,
+                                             grp, np, wsc, codes, header);
     SRLU_CHECK_LAUNCH("k1s_sched_kernel<1>");
     return SRLU_OK;
 }

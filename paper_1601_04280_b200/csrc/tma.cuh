@@ -45,6 +45,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
         : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// wait with back-off: for hand-offs where the waiter would otherwise steal
+// issue slots from the warps doing the work it waits for
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, unsigned parity, unsigned ns = 64) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
+
 // global -> shared bulk copy of `bytes` (multiple of 16, both addresses
 // 16-byte aligned), completion counted on `bar` (transaction bytes)
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
