@@ -50,7 +50,7 @@ constexpr size_t kSmemMax = 232448 - 1024;
 constexpr int kHeader = 16;             // int32 header words
 
 struct Cfg {
-    int es, rb, bpt, c, nch, ns, ng, zpad, d2;
+    int es, rb, bpt, c, nch, ns, ng, zpad, d2, sorted, joint;
     int64_t stage_bytes, row_stride, xs_bytes, code_cap, smem;
     // workspace offsets (bytes)
     int64_t off_grp, off_np, off_wsched, off_codes, ws_bytes;
@@ -71,12 +71,11 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
         if ((int64_t)kGW * b >= groups) { bpt = b; break; }
     if (!bpt) return false;
     const int64_t row_bytes = n * es;
-    // measured on B200 (tools/k1_sweep.py): two rows per block from 16 KB
-    // rows up, stages of one row but at least 32 KB and at most 64 KB
+    // measured on B200 (tools/k1_sweep.py): two rows per block from 8 KB
+    // rows up, stages of up to 64 KB (longer chunks = fewer idle lane-steps)
     int rb = env_int("SRLU_K1_RB", row_bytes <= 8192 ? 4 : 2);
     if (rb != 1 && rb != 2 && rb != 4) return false;
-    const int64_t stage_target =
-        env_int("SRLU_K1_STAGE", (int)std::min<int64_t>(65536, std::max<int64_t>(32768, row_bytes)));
+    const int64_t stage_target = env_int("SRLU_K1_STAGE", 65536);
     int64_t cmax = stage_target / (rb * es);
     cmax &= ~31LL;
     if (cmax < 32) return false;
@@ -88,6 +87,12 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     f.es = es; f.rb = rb; f.bpt = bpt; f.c = (int)c; f.nch = (int)nch;
     f.ng = kGW * bpt; f.zpad = kZeroBytes / es;
     f.d2 = env_int("SRLU_K1_D", 2) >= 2 ? 2 : 1;
+    // several slots per lane: buckets sorted by count into groups (similar
+    // queues per warp step), heavy and light groups paired per warp (snake),
+    // each slot on its own step sequence.  One slot: consecutive buckets, so
+    // the FWHT stages h < 32 run on the accumulators directly.
+    f.sorted = env_int("SRLU_K1_SORT", bpt >= 2 ? 1 : 0) != 0;
+    f.joint = !f.sorted;
     f.row_stride = (c + f.zpad) * es;
     f.stage_bytes = rb * f.row_stride;
     f.xs_bytes = 2LL * rb * pad * 8;
@@ -107,7 +112,7 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     f.off_grp = al(kHeader * 4);
     f.off_np = al(f.off_grp + (int64_t)f.ng * 32 * 4);
     f.off_wsched = al(f.off_np + (int64_t)nch * f.ng * 4);
-    f.off_codes = al(f.off_wsched + (int64_t)nch * kGW * 8);
+    f.off_codes = al(f.off_wsched + (int64_t)nch * f.ng * 8);
     // a step advances >= 1 source of its group; pairs round up; slots of a
     // warp are padded to the longest: <= bpt * 16 * (n + 2 nch ng) words
     f.ws_bytes = f.off_codes + 64LL * bpt * (n + 2 * nch * (int64_t)f.ng) + 64;
@@ -121,10 +126,47 @@ __host__ __device__ inline int group_of(int w, int b) { return b * kGW + ((b & 1
 // ---------------------------------------------------------------------------
 // schedule construction
 
-// slot -> bucket (identity grouping of consecutive buckets; -1 = empty lane)
-__global__ void group_kernel(int l, int ng, int32_t *grp) {
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ng * 32; s += gridDim.x * blockDim.x)
-        grp[s] = s < l ? s : -1;
+// slot -> bucket (-1 = empty lane).  sorted: buckets in descending order of
+// their source count (stable), so that the 32 lanes of a group have similar
+// queue lengths (fewer idle lane-steps); the snake map group_of() then pairs
+// heavy and light groups in one warp.  Otherwise consecutive buckets.
+// One CTA of 1024 threads: counting sort on min(count, 1023).
+__global__ void __launch_bounds__(1024) group_kernel(const int32_t *__restrict__ bptr, int l,
+                                                     int ng, int sorted, int32_t *grp) {
+    __shared__ int hist[1024];
+    __shared__ int cursor[1024];
+    const int tid = threadIdx.x;
+    for (int s = tid; s < ng * 32; s += blockDim.x) grp[s] = (!sorted && s < l) ? s : -1;
+    if (!sorted) return;
+    hist[tid] = 0;
+    __syncthreads();
+    for (int t = tid; t < l; t += blockDim.x) atomicAdd(&hist[1023 - min(bptr[t + 1] - bptr[t], 1023)], 1);
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan (descending count = ascending key)
+        int run = 0;
+        for (int k = 0; k < 1024; ++k) {
+            cursor[k] = run;
+            run += hist[k];
+        }
+    }
+    __syncthreads();
+    // stable scatter: warp 0 walks the buckets in order, 32 at a time
+    if (tid < 32) {
+        const unsigned lt = (1u << tid) - 1u;
+        for (int t0 = 0; t0 < l; t0 += 32) {
+            const int t = t0 + tid;
+            const bool ok = t < l;
+            const int key = ok ? 1023 - min(bptr[t + 1] - bptr[t], 1023) : 1024 + tid;
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (ok) {
+                const int pos = cursor[key] + __popc(peers & lt);
+                grp[pos] = t;
+            }
+            __syncwarp();
+            if (ok && (peers & lt) == 0) cursor[key] += __popc(peers);
+            __syncwarp();
+        }
+    }
 }
 
 // One warp per group simulates the walk of its 32 lanes chunk by chunk: in
@@ -137,7 +179,7 @@ __global__ void group_kernel(int l, int ng, int32_t *grp) {
 template <int PASS>
 __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ sorted,
                                                    const int32_t *__restrict__ bptr, int c,
-                                                   int nch, int es8, int bpt, int d2,
+                                                   int nch, int es8, int bpt, int d2, int joint,
                                                    const int32_t *__restrict__ grp,
                                                    int32_t *np_tab, int32_t *wsched,
                                                    uint32_t *codes, int32_t *header) {
@@ -153,7 +195,7 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
     best[lane] = 0;
     best2[lane] = 0;
     __syncwarp();
-    auto joint = [&](int ch, int ww) {  // pairs of warp ww in chunk ch
+    auto joint_np = [&](int ch, int ww) {  // common pairs of warp ww in chunk ch
         int mx = 0;
         for (int bb = 0; bb < bpt; ++bb) mx = max(mx, np_tab[ch * ng + group_of(ww, bb)]);
         return mx;
@@ -162,14 +204,15 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
         const int c0 = ch * c, c1 = c0 + c;
         uint32_t *out = nullptr;
         int npj = 0;
-        if (PASS == 1) {
+        int pstride = 32;  // words between consecutive pairs of this group
+        if (PASS == 1 && joint) {
             // base of (ch, w): all (ch', w') before it in [chunk][warp] order
             const int idx = ch * kGW + w;
             int s = 0;
-            for (int i = lane; i < idx; i += 32) s += joint(i / kGW, i % kGW);
+            for (int i = lane; i < idx; i += 32) s += joint_np(i / kGW, i % kGW);
 #pragma unroll
             for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-            npj = joint(ch, w);
+            npj = joint_np(ch, w);
             const int base = s * bpt * 32;
             if (lane == 0 && b == 0) {
                 wsched[2 * idx] = base;
@@ -177,12 +220,28 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
                 if (idx == nch * kGW - 1) header[0] = base + npj * bpt * 32;
             }
             out = codes + base + b * 32 + lane;
+            pstride = bpt * 32;
+        } else if (PASS == 1) {
+            // base of (ch, g): all (ch', g') before it in [chunk][group] order
+            const int idx = ch * ng + g;
+            int s = 0;
+            for (int i = lane; i < idx; i += 32) s += np_tab[i];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+            npj = np_tab[idx];
+            const int base = s * 32;
+            if (lane == 0) {
+                wsched[2 * idx] = base;
+                wsched[2 * idx + 1] = npj;
+                if (idx == nch * ng - 1) header[0] = base + npj * 32;
+            }
+            out = codes + base + lane;
         }
         int step = 0;
         uint32_t pairw = 0;
         auto emit = [&](uint32_t code) {
             if (PASS == 1) {
-                if (step & 1) out[(size_t)(step >> 1) * bpt * 32] = pairw | (code << 16);
+                if (step & 1) out[(size_t)(step >> 1) * pstride] = pairw | (code << 16);
                 else pairw = code;
             }
             ++step;
@@ -237,7 +296,7 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
 // the sketch kernel
 
 struct Dev {
-    int c, nch, ns, ng, dbg;
+    int c, nch, ns, ng, dbg, pf, sorted, joint;
     int row_stride, stage_bytes;
     int xs_off, code_off, code_cap;
 };
@@ -275,15 +334,14 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
                                             const double *__restrict__ phase, const Dev &d,
                                             int64_t my_nrb, int64_t nitems, uint64_t *full,
                                             uint64_t *xs_full, uint64_t *xs_empty, unsigned *rel,
-                                            double *xs_base, int pad, const Issue &issue) {
+                                            double *xs_base, int pad, int l, const Issue &issue) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int gid[BPT];
+    int bt[BPT];
     bool bneg[BPT];
 #pragma unroll
     for (int b = 0; b < BPT; ++b) {
-        gid[b] = group_of(warp, b);
-        const int t = grp[gid[b] * 32 + lane];
-        bneg[b] = t >= 0 && phase[t] < 0.0;
+        bt[b] = grp[group_of(warp, b) * 32 + lane];
+        bneg[b] = bt[b] >= 0 && phase[bt[b]] < 0.0;
     }
     int stage = 0;
     unsigned ph = 0;
@@ -295,18 +353,33 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
 #pragma unroll
             for (int r = 0; r < RB; ++r) acc[b][r] = 0.0;
         for (int ch = 0; ch < d.nch; ++ch, ++it) {
-            const int2 sc = __ldg(wsched + ch * kGW + warp);
-            if (!(d.dbg & 8)) mbar_wait(&full[stage], ph);
+            if (!(d.dbg & 8)) mbar_wait_suspend(&full[stage], ph);
             const unsigned char *st = smem + stage * d.stage_bytes;
-            const int np = sc.y;
-            const int base = sc.x + lane;
+            if (BPT == 1 || d.joint) {
+                const int2 sc = __ldg(wsched + ch * kGW + warp);
+                const int np = sc.y;
+                const int base = sc.x + lane;
 #pragma unroll(BPT == 1 ? 4 : (BPT == 2 ? 2 : 1))
-            for (int s2 = 0; s2 < np; ++s2) {
+                for (int s2 = 0; s2 < np; ++s2) {
+#pragma unroll
+                    for (int b = 0; b < BPT; ++b) {
+                        const uint32_t w = cw[base + (s2 * BPT + b) * 32];
+                        gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
+                        gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
+                    }
+                }
+            } else {
 #pragma unroll
                 for (int b = 0; b < BPT; ++b) {
-                    const uint32_t w = cw[base + (s2 * BPT + b) * 32];
-                    gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
-                    gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
+                    const int2 sc = __ldg(wsched + ch * d.ng + group_of(warp, b));
+                    const int np = sc.y;
+                    const int base = sc.x + lane;
+#pragma unroll 4
+                    for (int s2 = 0; s2 < np; ++s2) {
+                        const uint32_t w = cw[base + s2 * 32];
+                        gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
+                        gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
+                    }
                 }
             }
             // release the stage; the last of the kGW warps refills it
@@ -327,13 +400,38 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
         const int buf = (int)(rbi & 1);
         if (rbi >= 2) mbar_wait_sleep(&xs_empty[buf], (unsigned)(((rbi >> 1) - 1) & 1), 256);
         double *xs = xs_base + (size_t)buf * RB * pad;
+        // +-phase, scatter by bucket, then (after all gather warps wrote) the
+        // FWHT stages h < 32 by shuffles on 32-aligned blocks of buckets;
+        // positions >= l (no bucket) enter as zeros
+        if (d.sorted) {
 #pragma unroll
-        for (int b = 0; b < BPT; ++b) {
-            const int pos = fwht_sw(gid[b] * 32 + lane);
+            for (int b = 0; b < BPT; ++b) {
+                if (bt[b] >= 0) {
+                    const int pos = fwht_sw(bt[b]);
 #pragma unroll
-            for (int r = 0; r < RB; ++r) {
-                const double v = fwht_lane_stages(bneg[b] ? -acc[b][r] : acc[b][r], lane);
-                if (gid[b] * 32 < pad) xs[r * pad + pos] = v;
+                    for (int r = 0; r < RB; ++r)
+                        xs[r * pad + pos] = bneg[b] ? -acc[b][r] : acc[b][r];
+                }
+            }
+            named_bar(2, kGW * 32);
+            for (int q = warp; q * 32 < l; q += kGW) {
+                const int pos = fwht_sw(q * 32 + lane);
+                const bool live = q * 32 + lane < l;
+#pragma unroll
+                for (int r = 0; r < RB; ++r)
+                    xs[r * pad + pos] = fwht_lane_stages(live ? xs[r * pad + pos] : 0.0, lane);
+            }
+        } else {
+            // consecutive buckets: slot g*32 + lane holds bucket g*32 + lane
+#pragma unroll
+            for (int b = 0; b < BPT; ++b) {
+                const int g = group_of(warp, b);
+                const int pos = fwht_sw(g * 32 + lane);
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    const double v = fwht_lane_stages(bneg[b] ? -acc[b][r] : acc[b][r], lane);
+                    if (g * 32 < pad) xs[r * pad + pos] = v;
+                }
             }
         }
         mbar_arrive(&xs_full[buf]);
@@ -392,6 +490,20 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
     uint64_t *fullp = full;
     const int nch = d.nch, cc = d.c, sbytes = d.stage_bytes, rstride = d.row_stride;
     const int64_t bid = blockIdx.x, gdim = gridDim.x;
+    const int pf = d.pf;
+    // item it -> (rows, column range) of A; PF > 0: also prefetch item it + PF
+    // into L2 so that the ring's bulk copies hit L2 (keeps more HBM bytes in
+    // flight than the shared-memory ring holds)
+    auto prefetch = [=](int64_t it) {
+        if (it >= nitems) return;
+        const int64_t rbi = it / nch;
+        const int ch = (int)(it - rbi * nch);
+        const int64_t row0 = (bid + rbi * gdim) * RB;
+        const int nrows = (int)min((int64_t)RB, m - row0);
+        const int64_t c0 = (int64_t)ch * cc;
+        const unsigned bytes = (unsigned)min((int64_t)cc, n - c0) * es;
+        for (int r = 0; r < nrows; ++r) bulk_prefetch_l2(a + (row0 + r) * lda + c0, bytes);
+    };
     auto issue = [=](int64_t it, int stage) {
         const int64_t rbi = it / nch;
         const int ch = (int)(it - rbi * nch);
@@ -404,17 +516,20 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
         mbar_arrive_expect_tx(&fullp[stage], bytes * nrows);
         for (int r = 0; r < nrows; ++r)
             bulk_g2s(st + (size_t)r * rstride, a + (row0 + r) * lda + c0, bytes, &fullp[stage]);
+        if (pf > 0) prefetch(it + pf);
     };
-    if (tid == 0 && !(d.dbg & 16))
+    if (tid == 0 && !(d.dbg & 16)) {
+        for (int64_t it = d.ns; pf > 0 && it < d.ns + pf - 1; ++it) prefetch(it);
         for (int64_t it = 0; it < d.ns && it < nitems; ++it) issue(it, (int)it);
+    }
 
     if (warp < kGW) {
         if (codes_in_smem)
             gather_warp<T, RB, BPT>(smem, codes_s, grp, wsched, phase, d, my_nrb, nitems, full,
-                                    xs_full, xs_empty, rel, xs_base, pad, issue);
+                                    xs_full, xs_empty, rel, xs_base, pad, l, issue);
         else
             gather_warp<T, RB, BPT>(smem, codes_g, grp, wsched, phase, d, my_nrb, nitems, full,
-                                    xs_full, xs_empty, rel, xs_base, pad, issue);
+                                    xs_full, xs_empty, rel, xs_base, pad, l, issue);
         return;
     }
     // ---------------------------------------------------------------- epilogue
@@ -461,7 +576,7 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
         named_bar(1, kEW * 32);
         // positions in [ng*32, nzb*bsize) are not rewritten by the gather
         // warps but were transformed in place: re-zero them
-        const int z0 = d.ng * 32, z1 = nzb * bsize;
+        const int z0 = d.sorted ? (l + 31) / 32 * 32 : d.ng * 32, z1 = nzb * bsize;
         for (int i = etid; z1 > z0 && i < RB * (z1 - z0); i += kEW * 32) {
             const int r = i / (z1 - z0), t = z0 + i % (z1 - z0);
             xs[(size_t)r * pad + fwht_sw(t)] = 0.0;
@@ -478,6 +593,8 @@ static int launch(const Cfg &f, const T *a, int64_t m, int64_t n, int64_t lda,
                   cudaStream_t s) {
     Dev d;
     d.c = f.c; d.nch = f.nch; d.ns = f.ns; d.ng = f.ng;
+    d.sorted = f.sorted; d.joint = f.joint;
+    d.pf = env_int("SRLU_K1_PF", 0);  // L2 prefetch distance in ring items (measured: no gain)
     d.dbg = env_int("SRLU_K1_DBG", 0);  // experiments: 1 no FWHT, 2 no outputs, 8 no waits
     d.row_stride = (int)f.row_stride; d.stage_bytes = (int)f.stage_bytes;
     d.xs_off = (int)(f.ns * f.stage_bytes);
@@ -557,14 +674,13 @@ extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, in
     int32_t *np = (int32_t *)(ws + f.off_np);
     int32_t *wsc = (int32_t *)(ws + f.off_wsched);
     uint32_t *codes = (uint32_t *)(ws + f.off_codes);
-    k1s::group_kernel<<<(unsigned)ceil_div((int64_t)f.ng * 32, 256), 256, 0, s>>>((int)l1, f.ng,
-                                                                                 grp);
+    k1s::group_kernel<<<1, 1024, 0, s>>>(bptr1, (int)l1, f.ng, f.sorted, grp);
     SRLU_CHECK_LAUNCH("k1s_group_kernel");
     k1s::sched_kernel<0><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.bpt, f.d2,
-                                             grp, np, wsc, codes, header);
+                                             f.joint, grp, np, wsc, codes, header);
     SRLU_CHECK_LAUNCH("k1s_sched_kernel<0>");
     k1s::sched_kernel<1><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.bpt, f.d2,
-                                             grp, np, wsc, codes, header);
+                                             f.joint, grp, np, wsc, codes, header);
     SRLU_CHECK_LAUNCH("k1s_sched_kernel<1>");
     return SRLU_OK;
 }

@@ -59,6 +59,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
     return ok != 0;
 }
 
+// blocking wait that suspends the warp in hardware until the phase flips
+// (suspend-time hint), instead of spinning on try_wait
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+
+// L2 prefetch of a global range (bulk, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // wait with back-off: for hand-offs where the waiter would otherwise steal
 // issue slots from the warps doing the work it waits for
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, unsigned parity, unsigned ns = 64) {
