@@ -68,11 +68,17 @@ __device__ __forceinline__ void fwht_block_warp(double *blk, int lane) {
 
 // Stages h = 1..16 of one value per lane (index j = 32*q + lane): the
 // reference's butterflies (a + b, a - b), lower index first, via shuffles.
+// Lower lane: v + p; upper lane: p - v.  Both are fma(s, v, p) with
+// s = +-1 (the product is exact, one rounding: bit-identical to the add).
+__device__ __forceinline__ double pm_one(bool neg) {
+    return __hiloint2double(neg ? (int)0xBFF00000 : 0x3FF00000, 0);
+}
+
 __device__ __forceinline__ double fwht_lane_stages(double v, int lane) {
 #pragma unroll
     for (int h = 1; h < 32; h <<= 1) {
         const double p = __shfl_xor_sync(0xffffffffu, v, h);
-        v = (lane & h) ? __dsub_rn(p, v) : __dadd_rn(v, p);
+        v = __fma_rn(pm_one(lane & h), v, p);
     }
     return v;
 }
@@ -176,10 +182,9 @@ __device__ __forceinline__ double wht_pick(const double *row, int bsize, int o, 
     for (int b = 0; b < NB; ++b) u[b] = row[b * bsize + o];
 #pragma unroll
     for (int s = 1, lvl = 0; s < NB; s <<= 1, ++lvl) {
-        const bool neg = (B >> lvl) & 1;
+        const double sg = pm_one((B >> lvl) & 1);
 #pragma unroll
-        for (int i = 0; i < NB / (2 * s); ++i)
-            u[i] = neg ? __dsub_rn(u[2 * i], u[2 * i + 1]) : __dadd_rn(u[2 * i], u[2 * i + 1]);
+        for (int i = 0; i < NB / (2 * s); ++i) u[i] = __fma_rn(sg, u[2 * i + 1], u[2 * i]);
     }
     return u[0];
 }

@@ -62,20 +62,10 @@ static int env_int(const char *name, int dflt) {
 }
 
 // Deterministic from (n, l, pad, es): the schedule and the kernel agree.
-static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
-    if (getenv("SRLU_K1_NOSCHED") != nullptr) return false;
-    if (pad < 32 || pad > 8192 || l < 1 || l > pad || n < 1) return false;
-    const int64_t groups = ceil_div(l, 32);
-    int bpt = 0;
-    for (int b : {1, 2, 4})
-        if ((int64_t)kGW * b >= groups) { bpt = b; break; }
-    if (!bpt) return false;
-    const int64_t row_bytes = n * es;
-    // measured on B200 (tools/k1_sweep.py): two rows per block from 8 KB
-    // rows up, stages of up to 64 KB (longer chunks = fewer idle lane-steps)
-    int rb = env_int("SRLU_K1_RB", row_bytes <= 8192 ? 4 : 2);
-    if (rb != 1 && rb != 2 && rb != 4) return false;
-    const int64_t stage_target = env_int("SRLU_K1_STAGE", 65536);
+// One geometry (rows per block rb, stage target bytes); false if it does
+// not fit the shared-memory budget with at least two stages.
+static bool config_try(int64_t n, int64_t l, int64_t pad, int es, int bpt, int rb,
+                       int64_t stage_target, Cfg *cf) {
     int64_t cmax = stage_target / (rb * es);
     cmax &= ~31LL;
     if (cmax < 32) return false;
@@ -104,10 +94,10 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     while (ns > 2 && (size_t)(ns * f.stage_bytes + f.xs_bytes + code_est) > kSmemMax) --ns;
     f.ns = ns;
     int64_t used = ns * f.stage_bytes + f.xs_bytes;
-    if ((size_t)used > kSmemMax) return false;
+    if ((size_t)used + 8192 > kSmemMax) return false;
     f.code_cap = ((int64_t)kSmemMax - used) & ~15LL;
     f.smem = used + f.code_cap;
-    // workspace: header | grp[ng*32] | np[nch*ng] | wsched[nch*kGW*2] | codes
+    // workspace: header | grp[ng*32] | np[nch*ng] | wsched[nch*ng*2] | codes
     auto al = [](int64_t v) { return (v + 15) & ~15LL; };
     f.off_grp = al(kHeader * 4);
     f.off_np = al(f.off_grp + (int64_t)f.ng * 32 * 4);
@@ -118,6 +108,33 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     f.ws_bytes = f.off_codes + 64LL * bpt * (n + 2 * nch * (int64_t)f.ng) + 64;
     *cf = f;
     return true;
+}
+
+// Deterministic from (n, l, pad, es): the schedule and the kernel agree.
+// Preferred geometry (measured on B200, tools/k1_sweep.py): two rows per
+// block from 8 KB rows up (four below), stages of up to 64 KB (longer chunks
+// = fewer idle lane-steps); smaller blocks/stages when the FWHT scratch of a
+// long transform leaves no room.
+static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
+    if (getenv("SRLU_K1_NOSCHED") != nullptr) return false;
+    if (pad < 32 || pad > 8192 || l < 1 || l > pad || n < 1) return false;
+    const int64_t groups = ceil_div(l, 32);
+    int bpt = 0;
+    for (int b : {1, 2, 4})
+        if ((int64_t)kGW * b >= groups) { bpt = b; break; }
+    if (!bpt) return false;
+    const int64_t row_bytes = n * es;
+    const int rb_env = env_int("SRLU_K1_RB", 0);
+    const int st_env = env_int("SRLU_K1_STAGE", 0);
+    if (rb_env || st_env) {
+        const int rb = rb_env ? rb_env : (row_bytes <= 8192 ? 4 : 2);
+        if (rb != 1 && rb != 2 && rb != 4) return false;
+        return config_try(n, l, pad, es, bpt, rb, st_env ? st_env : 65536, cf);
+    }
+    for (int rb = row_bytes <= 8192 ? 4 : 2; rb >= 1; rb >>= 1)
+        for (int64_t st = 65536; st >= 16384; st >>= 1)
+            if (config_try(n, l, pad, es, bpt, rb, st, cf)) return true;
+    return false;
 }
 
 // warp w, slot b -> group (snake order over the slots)
@@ -308,18 +325,15 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 template <typename T, int RB>
 __device__ __forceinline__ void gather_step(const unsigned char *st, int row_stride, uint32_t c,
                                             double (&acc)[RB]) {
+    // acc + s*v as fma(s, v, acc), s = +-1: exact product, one rounding —
+    // bit-identical to the reference's out += s * a
     const uint32_t col = c & 0x7fffu;
-    const uint32_t sg = (c & 0x8000u) << 16;
+    const double s = __hiloint2double((int)(((c & 0x8000u) << 16) | 0x3FF00000u), 0);
     const unsigned char *p = st + col * sizeof(T);
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-        if constexpr (sizeof(T) == 4) {
-            const uint32_t bits = *reinterpret_cast<const uint32_t *>(p + r * row_stride) ^ sg;
-            acc[r] = __dadd_rn(acc[r], (double)__uint_as_float(bits));
-        } else {
-            const uint2 bits = *reinterpret_cast<const uint2 *>(p + r * row_stride);
-            acc[r] = __dadd_rn(acc[r], __hiloint2double((int)(bits.y ^ sg), (int)bits.x));
-        }
+        const double v = (double)*reinterpret_cast<const T *>(p + r * row_stride);
+        acc[r] = __fma_rn(s, v, acc[r]);
     }
 }
 
