@@ -11,6 +11,9 @@
 // k2-row subsample, writing (Omega2 P A)^T (n x k2).  Only the l2 x n
 // bucket matrix S (about 6% of A's bytes at the BASELINE configs) makes a
 // round trip, mostly through L2.
+#include <stdlib.h>
+
+#include "async_copy.cuh"
 #include "fwht.cuh"
 #include "fwht_warp.cuh"
 
@@ -160,6 +163,93 @@ __global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ 
     }
 }
 
+// K3b v3: one CTA per 32 columns.  The tile x[t][c] (row stride 34) stays
+// in shared memory; the FWHT down t runs in register passes of up to four
+// stages: a warp item holds, for its 32 columns (lanes), the 16 values
+// t = base + j*h0 of one butterfly group, so loads/stores are conflict-free
+// and no transpose is needed.  The tile arrives by cp.async (all in flight);
+// the first pass applies
+// +-phase; the output pass reads the k sampled rows and writes Y^T rows.
+constexpr int kK3bLD = 34;  // row stride (doubles): 16-byte rows for cp.async
+
+template <int E>
+__device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int h0,
+                                         const double *__restrict__ phase, bool first) {
+    constexpr int LD = kK3bLD;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int items = pad / E;
+    for (int it = warp; it < items; it += nw) {
+        const int base = (it % h0) + (it / h0) * E * h0;
+        double v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const int t = base + j * h0;
+            double x = t < l ? xs[t * LD + lane] : 0.0;
+            if (first && t < l && phase[t] < 0.0) x = -x;
+            v[j] = x;
+        }
+#pragma unroll
+        for (int hh = 1; hh < E; hh <<= 1) {
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                if ((j & hh) == 0) {
+                    const double a = v[j], b = v[j + hh];
+                    v[j] = __dadd_rn(a, b);
+                    v[j + hh] = __dsub_rn(a, b);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < E; ++j) xs[(base + j * h0) * LD + lane] = v[j];
+    }
+}
+
+__global__ void __launch_bounds__(512) k3b_v3_kernel(const double *__restrict__ S, int64_t n,
+                                                     int l, int pad,
+                                                     const double *__restrict__ phase,
+                                                     const int32_t *__restrict__ idx, int k,
+                                                     double mult, double *__restrict__ out,
+                                                     int64_t ldo) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xs = reinterpret_cast<double *>(smem_raw);
+    constexpr int LD = kK3bLD;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+    const int nc = (int)((n - c0) < 32 ? (n - c0) : 32);
+    // the l x 32 tile of S, all in flight at once (cp.async, 16 B per copy;
+    // columns past n zero-filled)
+    for (int w = threadIdx.x; w < l * 16; w += blockDim.x) {
+        const int t = w >> 4, q = (w & 15) * 2;
+        const bool ok = q < nc && ((n & 1) == 0 || q + 1 < nc);
+        if (ok) {
+            cp_async_16(xs + t * LD + q, S + (int64_t)t * n + c0 + q, true);
+        } else {
+            xs[t * LD + q] = q < nc ? S[(int64_t)t * n + c0 + q] : 0.0;
+            xs[t * LD + q + 1] = q + 1 < nc ? S[(int64_t)t * n + c0 + q + 1] : 0.0;
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    bool first = true;
+    for (int h0 = 1; h0 < pad;) {
+        const int e = pad / h0 >= 16 ? 16 : pad / h0;
+        switch (e) {
+            case 16: k3b_pass<16>(xs, l, pad, h0, phase, first); break;
+            case 8: k3b_pass<8>(xs, l, pad, h0, phase, first); break;
+            case 4: k3b_pass<4>(xs, l, pad, h0, phase, first); break;
+            default: k3b_pass<2>(xs, l, pad, h0, phase, first); break;
+        }
+        first = false;
+        h0 *= e;
+        __syncthreads();
+    }
+    // sample and scale: warp per column, lanes over the k outputs
+    for (int c = warp; c < nc; c += nw)
+        for (int kk = lane; kk < k; kk += 32)
+            out[(c0 + c) * ldo + kk] = __dmul_rn(xs[idx[kk] * LD + c], mult);
+}
+
 template <typename T>
 static int launch_k3a(const T *a, int64_t rows, int64_t n, int64_t lda, const int32_t *member_row,
                       const double *member_sign, const int32_t *bptr, int64_t l2, double *S,
@@ -183,6 +273,16 @@ static int launch_k3a(const T *a, int64_t rows, int64_t n, int64_t lda, const in
 int launch_k3b(const double *S, int64_t n, int64_t l2, int64_t pad2, const double *phase2,
                const int32_t *idx2, int64_t k2, double mult2, double *out, int64_t ldo,
                cudaStream_t stream) {
+    if (pad2 >= 32 && pad2 * kK3bLD * 8 <= 200 * 1024 && getenv("SRLU_K3B_V2") == nullptr) {
+        const size_t smem = (size_t)pad2 * kK3bLD * 8;
+        SRLU_CUDA(cudaFuncSetAttribute(k3b_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        const int nt = pad2 >= 512 ? 512 : 256;
+        k3b_v3_kernel<<<(unsigned)ceil_div(n, 32), nt, smem, stream>>>(
+            S, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo);
+        SRLU_CHECK_LAUNCH("k3b_v3_kernel");
+        return SRLU_OK;
+    }
     if (pad2 >= 32 && pad2 <= 8192) {
         int CB = (int)(16384 / pad2);  // ~128 KB of smem
         if (CB < 1) CB = 1;

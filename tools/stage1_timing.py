@@ -1,43 +1,41 @@
-"""GPU span of the Omega1 build (draws + plan) vs K1 inside sketch1 (config 2)."""
-import os, sys
+"""Stage-1 breakdown (config N): host enqueue time and GPU span of the
+composite draws+plan, the K1 gather schedule and K1 itself, as in _attempt."""
+import os
+import sys
+import time
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
+
 import bench
 import paper_1601_04280_b200 as P
-from paper_1601_04280_b200.sketch import build_composite, sketch_right_into, transform_kind_for_field
+from paper_1601_04280_b200.sketch import build_composite, sketch_right_into
 
-a, prm = bench.gen_config(2)
-A = P.Matrix.from_device(a)
-params = P.RandLuParams(**prm)
-kind = transform_kind_for_field(params.field)
-res = []
+c = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+a, prm = bench.gen_config(c)
+cfg = bench.CONFIGS[c]
+A = bench.as_matrix(P, a, (cfg["m"], cfg["n"]))
+y = torch.empty(cfg["m"], prm["k1"], dtype=torch.float64, device="cuda")
+flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+rows = []
 for it in range(8):
     torch.cuda.synchronize()
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    e[0].record()
-    om1 = build_composite(params.k1, params.l1, A.shape[1], kind, params.seed, A.device)
-    e[1].record()
-    e[2].record()
-    y = torch.empty(A.shape[0], params.k1, dtype=torch.float64, device="cuda")
-    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
-    sketch_right_into(A, om1, y, flag)
-    e[3].record()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    h0 = time.perf_counter()
+    ev[0].record()
+    om = build_composite(prm["k1"], prm["l1"], cfg["n"], "hadamard", it, "cuda")
+    h1 = time.perf_counter()
+    ev[1].record()
+    om.sem.k1_schedule(P._lib.dtype_code(A.raw.dtype), om.fast.pad) if not A.is_sparse else None
+    h2 = time.perf_counter()
+    ev[2].record()
+    sketch_right_into(A, om, y, flag)
+    h3 = time.perf_counter()
+    ev[3].record()
     torch.cuda.synchronize()
-    res.append([e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])])
-r = np.median(np.array(res[2:]), axis=0) * 1e3
-print("build_composite %.1f us  - %.1f  K1 (incl. y alloc) %.1f us" % tuple(r))
-
-# host enqueue time of the one-call build
-import time
-hs = []
-for it in range(20):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    om = build_composite(params.k1, params.l1, A.shape[1], kind, params.seed, A.device)
-    t1 = time.perf_counter()
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    hs.append([t1 - t0, t2 - t1])
-h = np.median(np.array(hs[3:]), axis=0) * 1e6
-print("host us: build_composite %.1f  then GPU drain %.1f" % tuple(h))
+    rows.append([(h1 - h0) * 1e3, (h2 - h1) * 1e3, (h3 - h2) * 1e3,
+                 ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
+r = np.median(np.array(rows[2:]), axis=0)
+print(f"config {c}: host ms composite {r[0]:.3f} sched {r[1]:.3f} k1-call {r[2]:.3f} | "
+      f"gpu ms composite {r[3]:.3f} sched {r[4]:.3f} k1 {r[5]:.3f}")
