@@ -55,27 +55,36 @@ __global__ void plan_scan_blocks_kernel(int *counts, int nblk, int l, int *total
     if (threadIdx.x == 0) total[t] = carry;
 }
 
-// single CTA: bucket_ptr = exclusive scan of totals
-__global__ void plan_scan_buckets_kernel(const int *total, int l, int32_t *bucket_ptr) {
-    __shared__ int part[1024];
-    int nt = blockDim.x;
-    int per = (l + nt - 1) / nt;
-    int lo = threadIdx.x * per, hi = min(l, lo + per);
+// single CTA: bucket_ptr = exclusive scan of totals (per-thread run, then a
+// warp-shuffle block scan of the 1024 partial sums)
+__global__ void __launch_bounds__(1024) plan_scan_buckets_kernel(const int *total, int l,
+                                                                 int32_t *bucket_ptr) {
+    __shared__ int wsum[32];
+    const int nt = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (l + nt - 1) / nt;
+    const int lo = threadIdx.x * per, hi = min(l, lo + per);
     int s = 0;
     for (int t = lo; t < hi; ++t) s += total[t];
-    part[threadIdx.x] = s;
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int i = 0; i < nt; ++i) {
-            int c = part[i];
-            part[i] = run;
-            run += c;
+    if (warp == 0) {
+        int w = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += v;
         }
-        bucket_ptr[l] = run;
+        wsum[lane] = w;  // inclusive over warps
     }
     __syncthreads();
-    int run = part[threadIdx.x];
+    int run = incl - s + (warp ? wsum[warp - 1] : 0);
+    if (threadIdx.x == nt - 1) bucket_ptr[l] = run + s;
     for (int t = lo; t < hi; ++t) {
         bucket_ptr[t] = run;
         run += total[t];
@@ -94,17 +103,28 @@ __global__ void plan_scatter_kernel(const int32_t *row_of, const double *sign, i
     int64_t b0 = (int64_t)blockIdx.x * kPlanBlock;
     int64_t b1 = min(n, b0 + kPlanBlock);
     unsigned lt_mask = (1u << lane) - 1u;
-    for (int64_t c = b0; c < b1; c += 32) {
-        int64_t i = c + lane;
+    // all of the block's draws in flight at once (kPlanBlock / 32 per lane)
+    constexpr int NC = kPlanBlock / 32;
+    int tv[NC];
+    bool neg[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        const int64_t i = b0 + q * 32 + lane;
+        tv[q] = i < b1 ? row_of[i] : 0;
+        neg[q] = i < b1 ? sign[i] < 0.0 : false;
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        int64_t i = b0 + q * 32 + lane;
         bool valid = i < b1;
         unsigned active = __ballot_sync(0xffffffffu, valid);
         if (valid) {
-            int t = row_of[i];
+            int t = tv[q];
             unsigned peers = __match_any_sync(active, t);
             int rank = __popc(peers & lt_mask);
             int base = cursor[t];
             __syncwarp(active);
-            int32_t code = (int32_t)i | (sign[i] < 0.0 ? (int32_t)0x80000000 : 0);
+            int32_t code = (int32_t)i | (neg[q] ? (int32_t)0x80000000 : 0);
             sorted[base + rank] = code;
             if (rank == 0) cursor[t] = base + __popc(peers);
         }

@@ -184,7 +184,9 @@ __device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int h0,
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const int t = base + j * h0;
-            double x = t < l ? xs[t * LD + lane] : 0.0;
+            // first pass: rows t >= l were never loaded (zero); later passes
+            // read the in-place results of the previous one
+            double x = (!first || t < l) ? xs[t * LD + lane] : 0.0;
             if (first && t < l && phase[t] < 0.0) x = -x;
             v[j] = x;
         }
@@ -220,7 +222,8 @@ __global__ void __launch_bounds__(512) k3b_v3_kernel(const double *__restrict__ 
     // columns past n zero-filled)
     for (int w = threadIdx.x; w < l * 16; w += blockDim.x) {
         const int t = w >> 4, q = (w & 15) * 2;
-        const bool ok = q < nc && ((n & 1) == 0 || q + 1 < nc);
+        // 16-byte copies need an even row pitch (S + t*n + c0 + q aligned)
+        const bool ok = (n & 1) == 0 && q + 1 < nc;
         if (ok) {
             cp_async_16(xs + t * LD + q, S + (int64_t)t * n + c0 + q, true);
         } else {

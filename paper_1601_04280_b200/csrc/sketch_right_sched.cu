@@ -193,25 +193,21 @@ __global__ void __launch_bounds__(1024) group_kernel(const int32_t *__restrict__
 // PASS 0 counts step pairs per (chunk, group).  PASS 1 pads the slots of each
 // warp to a common pair count per chunk and writes the codes at
 // [chunk][warp][pair][slot][lane] (u32 = two 16-bit codes).
+constexpr int kSchedListCap = 4096;  // staged source codes per group (ints)
+
+// One pass of the simulation for group g (see sched_kernel).  src[0..cnt) =
+// this lane's bucket sources (ascending, sign in bit 31).
 template <int PASS>
-__global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ sorted,
-                                                   const int32_t *__restrict__ bptr, int c,
-                                                   int nch, int es8, int bpt, int d2, int joint,
-                                                   const int32_t *__restrict__ grp,
-                                                   int32_t *np_tab, int32_t *wsched,
-                                                   uint32_t *codes, int32_t *header) {
-    __shared__ unsigned best[32], best2[32];
-    const int g = blockIdx.x, lane = threadIdx.x;
+__device__ __forceinline__ void sched_pass(const int32_t *src, int cnt, int g, int c, int nch,
+                                           int es8, int bpt, int d2, int joint, int32_t *np_tab,
+                                           int32_t *wsched, uint32_t *codes, int32_t *header,
+                                           unsigned *best, unsigned *best2) {
+    const int lane = threadIdx.x;
     const int ng = kGW * bpt;
     const int b = g / kGW, w = (b & 1) ? kGW - 1 - (g % kGW) : (g % kGW);
     const unsigned FULL = 0xffffffffu;
-    const int t = grp[g * 32 + lane];
-    int cur = t >= 0 ? bptr[t] : 0;
-    const int end = t >= 0 ? bptr[t + 1] : 0;
-    int nxt = cur < end ? sorted[cur] : INT_MAX;
-    best[lane] = 0;
-    best2[lane] = 0;
-    __syncwarp();
+    int cur = 0;
+    int nxt = cnt > 0 ? src[0] : INT_MAX;
     auto joint_np = [&](int ch, int ww) {  // common pairs of warp ww in chunk ch
         int mx = 0;
         for (int bb = 0; bb < bpt; ++bb) mx = max(mx, np_tab[ch * ng + group_of(ww, bb)]);
@@ -269,7 +265,7 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
             if (!__any_sync(FULL, pend)) break;
             const int lc = col - c0;
             const int key = es8 ? ((lc & 15) | (lane & 16)) : (lc & 31);
-            const int rem = end - cur;
+            const int rem = cnt - cur;
             const unsigned prio = ((unsigned)min(rem, 1 << 20) << 5) | (unsigned)(31 - lane);
             if (pend) atomicMax(&best[key], prio);
             __syncwarp();
@@ -297,7 +293,7 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
             emit(code);
             if (win) {
                 ++cur;
-                nxt = cur < end ? __ldg(sorted + cur) : INT_MAX;
+                nxt = cur < cnt ? src[cur] : INT_MAX;
             }
             __syncwarp();
         }
@@ -307,6 +303,56 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
         while (step < target) emit((uint32_t)c);
         if (PASS == 0 && lane == 0) np_tab[ch * ng + g] = step >> 1;
     }
+}
+
+// One warp (CTA) per group simulates the walk of its 32 lanes chunk by
+// chunk: in each step every pending lane proposes its next source; per bank
+// (per half-warp bank pair for 8-byte elements) the D lanes with the longest
+// remaining queue win, the others read a zero word in a bank nobody uses.
+// Pass 0 counts step pairs per (chunk, group); after a grid barrier (cooperative
+// launch) pass 1 lays the codes out: joint = the slots of each warp padded to
+// a common pair count per chunk, [chunk][warp][pair][slot][lane]; otherwise
+// [chunk][group][pair][lane].  u32 = two 16-bit codes.  The group's source
+// lists are staged in shared memory when they fit.
+__global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ sorted,
+                                                   const int32_t *__restrict__ bptr, int l, int c,
+                                                   int nch, int es8, int bpt, int d2, int joint,
+                                                   const int32_t *__restrict__ grp,
+                                                   int32_t *np_tab, int32_t *wsched,
+                                                   uint32_t *codes, int32_t *header,
+                                                   unsigned *barrier) {
+    __shared__ unsigned best[32], best2[32];
+    __shared__ int32_t lists[kSchedListCap];
+    const int g = blockIdx.x, lane = threadIdx.x;
+    const unsigned FULL = 0xffffffffu;
+    const int t = grp ? grp[g * 32 + lane] : (g * 32 + lane < l ? g * 32 + lane : -1);
+    const int beg = t >= 0 ? bptr[t] : 0;
+    const int cnt = t >= 0 ? bptr[t + 1] - beg : 0;
+    int off = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, off, o);
+        if (lane >= o) off += v;
+    }
+    const int total = __shfl_sync(FULL, off, 31);
+    off -= cnt;
+    const bool staged = total <= kSchedListCap;
+    if (staged) {
+        for (int j = 0; j < 32; ++j) {
+            const int bj = __shfl_sync(FULL, beg, j), nj = __shfl_sync(FULL, cnt, j);
+            const int oj = __shfl_sync(FULL, off, j);
+            for (int i = lane; i < nj; i += 32) lists[oj + i] = __ldg(sorted + bj + i);
+        }
+    }
+    best[lane] = 0;
+    best2[lane] = 0;
+    __syncwarp();
+    const int32_t *src = staged ? lists + off : sorted + beg;
+    sched_pass<0>(src, cnt, g, c, nch, es8, bpt, d2, joint, np_tab, wsched, codes, header, best,
+                  best2);
+    grid_arrive_wait(barrier, gridDim.x);
+    sched_pass<1>(src, cnt, g, c, nch, es8, bpt, d2, joint, np_tab, wsched, codes, header, best,
+                  best2);
 }
 
 // ---------------------------------------------------------------------------
@@ -354,7 +400,8 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
     bool bneg[BPT];
 #pragma unroll
     for (int b = 0; b < BPT; ++b) {
-        bt[b] = grp[group_of(warp, b) * 32 + lane];
+        const int slot = group_of(warp, b) * 32 + lane;
+        bt[b] = d.sorted ? grp[slot] : (slot < l ? slot : -1);
         bneg[b] = bt[b] >= 0 && phase[bt[b]] < 0.0;
     }
     int stage = 0;
@@ -688,14 +735,21 @@ extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, in
     int32_t *np = (int32_t *)(ws + f.off_np);
     int32_t *wsc = (int32_t *)(ws + f.off_wsched);
     uint32_t *codes = (uint32_t *)(ws + f.off_codes);
-    k1s::group_kernel<<<1, 1024, 0, s>>>(bptr1, (int)l1, f.ng, f.sorted, grp);
-    SRLU_CHECK_LAUNCH("k1s_group_kernel");
-    k1s::sched_kernel<0><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.bpt, f.d2,
-                                             f.joint, grp, np, wsc, codes, header);
-    SRLU_CHECK_LAUNCH("k1s_sched_kernel<0>");
-    k1s::sched_kernel<1><<<f.ng, 32, 0, s>>>(sorted1, bptr1, f.c, f.nch, es == 8, f.bpt, f.d2,
-                                             f.joint, grp, np, wsc, codes, header);
-    SRLU_CHECK_LAUNCH("k1s_sched_kernel<1>");
+    if (f.sorted) {
+        k1s::group_kernel<<<1, 1024, 0, s>>>(bptr1, (int)l1, f.ng, f.sorted, grp);
+        SRLU_CHECK_LAUNCH("k1s_group_kernel");
+    }
+    SRLU_CUDA(cudaMemsetAsync(header, 0, k1s::kHeader * sizeof(int32_t), s));
+    const int32_t *grp_arg = f.sorted ? grp : nullptr;
+    int l_arg = (int)l1, c_arg = f.c, nch_arg = f.nch, es8 = es == 8, bpt_arg = f.bpt,
+        d2_arg = f.d2, joint_arg = f.joint;
+    unsigned *bar = (unsigned *)(header + 1);
+    void *args[] = {(void *)&sorted1, (void *)&bptr1, &l_arg,   &c_arg, &nch_arg, &es8,
+                    &bpt_arg,         &d2_arg,        &joint_arg, (void *)&grp_arg, &np,
+                    &wsc,             &codes,         &header,  &bar};
+    SRLU_CUDA(cudaLaunchCooperativeKernel((const void *)k1s::sched_kernel, dim3(f.ng), dim3(32),
+                                          args, 0, s));
+    SRLU_CHECK_LAUNCH("k1s_sched_kernel");
     return SRLU_OK;
 }
 
