@@ -372,8 +372,8 @@ def main():
         else:
             mat = P.Matrix.from_device(host_a.to("cuda", non_blocking=True))
         r = P.sparse_randomized_lu(mat, params)
-        lh = r.L.to_dense().cpu()
-        uh = r.U.to_dense().cpu()
+        lh = r.L.to_host()  # pinned D2H through the public Matrix API
+        uh = r.U.to_host()
         d2h["bytes"] = lh.numel() * 8 + uh.numel() * 8 + r.P.size * 8 + r.Q.size * 8
 
     e2e_step()

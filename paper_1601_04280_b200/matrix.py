@@ -179,8 +179,23 @@ class Matrix:
         out[rows, self._indices.long()] = self._values
         return out
 
+    def to_host(self) -> torch.Tensor:
+        """Copy to page-locked host memory (full-speed DMA; the caching
+        host allocator reuses the buffers) and wait for it.  Keeps the
+        device tensor's strides (e.g. U, a transposed view), so the copy is
+        one contiguous transfer."""
+        t = self.to_dense()
+        if not t.is_cuda:
+            return t
+        if not t.is_contiguous() and not t.t().is_contiguous():
+            t = t.contiguous()
+        h = torch.empty_strided(t.size(), t.stride(), dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return h
+
     def numpy(self) -> np.ndarray:
-        return self.to_dense().double().cpu().numpy()
+        return self.to_host().double().numpy()
 
     def __repr__(self):
         kind = "csr" if self.is_sparse else "dense"
