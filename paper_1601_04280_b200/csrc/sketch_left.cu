@@ -170,15 +170,23 @@ __global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ 
 // and no transpose is needed.  The tile arrives by cp.async (all in flight);
 // the first pass applies
 // +-phase; the output pass reads the k sampled rows and writes Y^T rows.
-constexpr int kK3bLD = 34;  // row stride (doubles): 16-byte rows for cp.async
+// CB columns per CTA (16 or 32); row stride CB+2 doubles (16-byte rows for
+// cp.async, conflict-free row accesses).  A warp holds 32/CB items at once.
+template <int CB>
+struct K3bGeo {
+    static constexpr int LD = CB + 2;
+    static constexpr int SUB = 32 / CB;
+};
 
-template <int E>
+template <int CB, int E>
 __device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int h0,
                                          const double *__restrict__ phase, bool first) {
-    constexpr int LD = kK3bLD;
+    constexpr int LD = K3bGeo<CB>::LD, SUB = K3bGeo<CB>::SUB;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int col = lane % CB, sub = lane / CB;
     const int items = pad / E;
-    for (int it = warp; it < items; it += nw) {
+    for (int it0 = warp * SUB; it0 < items; it0 += nw * SUB) {
+        const int it = it0 + sub;
         const int base = (it % h0) + (it / h0) * E * h0;
         double v[E];
 #pragma unroll
@@ -186,7 +194,7 @@ __device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int h0,
             const int t = base + j * h0;
             // first pass: rows t >= l were never loaded (zero); later passes
             // read the in-place results of the previous one
-            double x = (!first || t < l) ? xs[t * LD + lane] : 0.0;
+            double x = (!first || t < l) ? xs[t * LD + col] : 0.0;
             if (first && t < l && phase[t] < 0.0) x = -x;
             v[j] = x;
         }
@@ -202,11 +210,12 @@ __device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int h0,
             }
         }
 #pragma unroll
-        for (int j = 0; j < E; ++j) xs[(base + j * h0) * LD + lane] = v[j];
+        for (int j = 0; j < E; ++j) xs[(base + j * h0) * LD + col] = v[j];
     }
 }
 
-__global__ void __launch_bounds__(512) k3b_v3_kernel(const double *__restrict__ S, int64_t n,
+template <int CB>
+__global__ void __launch_bounds__(256) k3b_v3_kernel(const double *__restrict__ S, int64_t n,
                                                      int l, int pad,
                                                      const double *__restrict__ phase,
                                                      const int32_t *__restrict__ idx, int k,
@@ -214,14 +223,14 @@ __global__ void __launch_bounds__(512) k3b_v3_kernel(const double *__restrict__ 
                                                      int64_t ldo) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *xs = reinterpret_cast<double *>(smem_raw);
-    constexpr int LD = kK3bLD;
+    constexpr int LD = K3bGeo<CB>::LD, Q = CB / 2;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t c0 = (int64_t)blockIdx.x * 32;
-    const int nc = (int)((n - c0) < 32 ? (n - c0) : 32);
-    // the l x 32 tile of S, all in flight at once (cp.async, 16 B per copy;
+    const int64_t c0 = (int64_t)blockIdx.x * CB;
+    const int nc = (int)((n - c0) < CB ? (n - c0) : CB);
+    // the l x CB tile of S, all in flight at once (cp.async, 16 B per copy;
     // columns past n zero-filled)
-    for (int w = threadIdx.x; w < l * 16; w += blockDim.x) {
-        const int t = w >> 4, q = (w & 15) * 2;
+    for (int w = threadIdx.x; w < l * Q; w += blockDim.x) {
+        const int t = w / Q, q = (w % Q) * 2;
         // 16-byte copies need an even row pitch (S + t*n + c0 + q aligned)
         const bool ok = (n & 1) == 0 && q + 1 < nc;
         if (ok) {
@@ -238,10 +247,10 @@ __global__ void __launch_bounds__(512) k3b_v3_kernel(const double *__restrict__ 
     for (int h0 = 1; h0 < pad;) {
         const int e = pad / h0 >= 16 ? 16 : pad / h0;
         switch (e) {
-            case 16: k3b_pass<16>(xs, l, pad, h0, phase, first); break;
-            case 8: k3b_pass<8>(xs, l, pad, h0, phase, first); break;
-            case 4: k3b_pass<4>(xs, l, pad, h0, phase, first); break;
-            default: k3b_pass<2>(xs, l, pad, h0, phase, first); break;
+            case 16: k3b_pass<CB, 16>(xs, l, pad, h0, phase, first); break;
+            case 8: k3b_pass<CB, 8>(xs, l, pad, h0, phase, first); break;
+            case 4: k3b_pass<CB, 4>(xs, l, pad, h0, phase, first); break;
+            default: k3b_pass<CB, 2>(xs, l, pad, h0, phase, first); break;
         }
         first = false;
         h0 *= e;
@@ -276,12 +285,15 @@ static int launch_k3a(const T *a, int64_t rows, int64_t n, int64_t lda, const in
 int launch_k3b(const double *S, int64_t n, int64_t l2, int64_t pad2, const double *phase2,
                const int32_t *idx2, int64_t k2, double mult2, double *out, int64_t ldo,
                cudaStream_t stream) {
-    if (pad2 >= 32 && pad2 * kK3bLD * 8 <= 200 * 1024 && getenv("SRLU_K3B_V2") == nullptr) {
-        const size_t smem = (size_t)pad2 * kK3bLD * 8;
-        SRLU_CUDA(cudaFuncSetAttribute(k3b_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-        const int nt = pad2 >= 512 ? 512 : 256;
-        k3b_v3_kernel<<<(unsigned)ceil_div(n, 32), nt, smem, stream>>>(
+    // v3: 16 columns per CTA when three CTAs then fit an SM, else 32
+    const int v3cb = getenv("SRLU_K3B_CB") ? atoi(getenv("SRLU_K3B_CB")) : 0;
+    if (pad2 >= 32 && getenv("SRLU_K3B_V2") == nullptr &&
+        ((v3cb != 32 && pad2 * 18 * 8 <= 75 * 1024) || pad2 * 34 * 8 <= 200 * 1024)) {
+        const bool cb16 = v3cb != 32 && pad2 * 18 * 8 <= 75 * 1024;
+        const size_t smem = (size_t)pad2 * (cb16 ? 18 : 34) * 8;
+        auto kern = cb16 ? k3b_v3_kernel<16> : k3b_v3_kernel<32>;
+        SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)ceil_div(n, cb16 ? 16 : 32), 256, smem, stream>>>(
             S, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo);
         SRLU_CHECK_LAUNCH("k3b_v3_kernel");
         return SRLU_OK;
