@@ -201,14 +201,18 @@ def flush_l2():
     _flush_buf.fill_(1)
 
 
-def time_region(fn, steps, flush=True, barrier=None):
+def time_region(fn, steps, flush=True, barrier=None, kernel=False):
     """Per-step CUDA-event times (ms) on the current stream; L2 flushed
-    before every step outside the timed span."""
+    before every step outside the timed span.  kernel=True (single-kernel
+    timings for the rooflines): the start event is enqueued behind the L2
+    flush without a host sync, so the host's launch latency overlaps the
+    flush instead of being counted as kernel time."""
     times = []
     for _ in range(steps):
         if flush:
             flush_l2()
-        torch.cuda.synchronize()
+        if not kernel:
+            torch.cuda.synchronize()
         if barrier:
             barrier()
         s = torch.cuda.Event(enable_timing=True)
@@ -336,7 +340,8 @@ def main():
     ops.omega1.sem.plan()
     sketch_right_into(A, ops.omega1, y, flag)  # builds the K1 gather schedule (once per sketch)
     k1_sched = any(v is not None for _, v in ops.omega1.sem._sched)
-    k1_times = time_region(lambda: sketch_right_into(A, ops.omega1, y, flag), args.steps)
+    k1_times = time_region(lambda: sketch_right_into(A, ops.omega1, y, flag), args.steps,
+                           kernel=True)
     k1_ms = float(np.mean(k1_times))
     k1_bytes = nbytes + y.numel() * 8
     # K3 (projection stream of P A)
@@ -350,7 +355,7 @@ def main():
     else:
         mrow, msign, bptr = members(ops.omega2, perm, 0, shape[0])
         k3 = lambda: sketch_left_into(A, ops.omega2, mrow, msign, bptr, out)
-    k3_ms = float(np.mean(time_region(k3, args.steps)))
+    k3_ms = float(np.mean(time_region(k3, args.steps, kernel=True)))
     k3_bytes = nbytes + out.numel() * 8
     peak, peak_src = measured_peaks()
     k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
