@@ -179,23 +179,25 @@ struct K3bGeo {
 };
 
 template <int CB, int E>
-__device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int h0,
-                                         const double *__restrict__ phase, bool first) {
+__device__ __forceinline__ void k3b_pass(double *xs, int l, int pad, int lh0,
+                                         const uint32_t *sgn, bool first) {
     constexpr int LD = K3bGeo<CB>::LD, SUB = K3bGeo<CB>::SUB;
+    constexpr int LE = E == 16 ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int col = lane % CB, sub = lane / CB;
-    const int items = pad / E;
+    const int items = pad >> LE;
+    const int h0 = 1 << lh0;
     for (int it0 = warp * SUB; it0 < items; it0 += nw * SUB) {
         const int it = it0 + sub;
-        const int base = (it % h0) + (it / h0) * E * h0;
+        const int base = (it & (h0 - 1)) + ((it >> lh0) << (LE + lh0));
         double v[E];
 #pragma unroll
         for (int j = 0; j < E; ++j) {
-            const int t = base + j * h0;
-            // first pass: rows t >= l were never loaded (zero); later passes
-            // read the in-place results of the previous one
+            const int t = base + (j << lh0);
+            // first pass: rows t >= l were never loaded (zero) and carry the
+            // +-phase sign; later passes read the in-place results
             double x = (!first || t < l) ? xs[t * LD + col] : 0.0;
-            if (first && t < l && phase[t] < 0.0) x = -x;
+            if (first) x = __hiloint2double(__double2hiint(x) ^ (int)sgn[t], __double2loint(x));
             v[j] = x;
         }
 #pragma unroll
@@ -240,20 +242,23 @@ __global__ void __launch_bounds__(256) k3b_v3_kernel(const double *__restrict__ 
             xs[t * LD + q + 1] = q + 1 < nc ? S[(int64_t)t * n + c0 + q + 1] : 0.0;
         }
     }
+    // sign bits of the phase (bit 31 of the high word), zero past l
+    uint32_t *sgn = reinterpret_cast<uint32_t *>(xs + (size_t)pad * LD);
+    for (int t = threadIdx.x; t < pad; t += blockDim.x)
+        sgn[t] = (t < l && phase[t] < 0.0) ? 0x80000000u : 0u;
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     bool first = true;
-    for (int h0 = 1; h0 < pad;) {
-        const int e = pad / h0 >= 16 ? 16 : pad / h0;
+    for (int lh0 = 0; (1 << lh0) < pad;) {
+        const int e = (pad >> lh0) >= 16 ? 16 : (pad >> lh0);
         switch (e) {
-            case 16: k3b_pass<CB, 16>(xs, l, pad, h0, phase, first); break;
-            case 8: k3b_pass<CB, 8>(xs, l, pad, h0, phase, first); break;
-            case 4: k3b_pass<CB, 4>(xs, l, pad, h0, phase, first); break;
-            default: k3b_pass<CB, 2>(xs, l, pad, h0, phase, first); break;
+            case 16: k3b_pass<CB, 16>(xs, l, pad, lh0, sgn, first); lh0 += 4; break;
+            case 8: k3b_pass<CB, 8>(xs, l, pad, lh0, sgn, first); lh0 += 3; break;
+            case 4: k3b_pass<CB, 4>(xs, l, pad, lh0, sgn, first); lh0 += 2; break;
+            default: k3b_pass<CB, 2>(xs, l, pad, lh0, sgn, first); lh0 += 1; break;
         }
         first = false;
-        h0 *= e;
         __syncthreads();
     }
     // sample and scale: warp per column, lanes over the k outputs
@@ -288,9 +293,9 @@ int launch_k3b(const double *S, int64_t n, int64_t l2, int64_t pad2, const doubl
     // v3: 16 columns per CTA when three CTAs then fit an SM, else 32
     const int v3cb = getenv("SRLU_K3B_CB") ? atoi(getenv("SRLU_K3B_CB")) : 0;
     if (pad2 >= 32 && getenv("SRLU_K3B_V2") == nullptr &&
-        ((v3cb != 32 && pad2 * 18 * 8 <= 75 * 1024) || pad2 * 34 * 8 <= 200 * 1024)) {
+        ((v3cb != 32 && pad2 * 18 * 8 <= 75 * 1024) || pad2 * 34 * 8 <= 196 * 1024)) {
         const bool cb16 = v3cb != 32 && pad2 * 18 * 8 <= 75 * 1024;
-        const size_t smem = (size_t)pad2 * (cb16 ? 18 : 34) * 8;
+        const size_t smem = (size_t)pad2 * (cb16 ? 18 : 34) * 8 + (size_t)pad2 * 4;
         auto kern = cb16 ? k3b_v3_kernel<16> : k3b_v3_kernel<32>;
         SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<(unsigned)ceil_div(n, cb16 ? 16 : 32), 256, smem, stream>>>(
