@@ -53,7 +53,8 @@ namespace srlu {
 
 enum { MODE_ROW = 0, MODE_COL = 1 };
 
-constexpr int kLuThreads = 256;
+constexpr int kLuThreads = 512;
+constexpr int kLuRPW = 4;  // trailing update: rows per warp pass
 constexpr int kLuMaxGrid = 256;
 constexpr int kLuXC = 64;  // trailing columns per chunk
 constexpr double kPivotRtol = 1e-14;  // factor.py:19
@@ -311,20 +312,47 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 }
             }
             __syncthreads();
-            for (int w = tid; w < ne * xc; w += blockDim.x) {
-                const int e = w / xc, c = w % xc;
-                if (pos[e] < J + bw) continue;  // pivots are frozen
-                double *gp = p.w + (e0 + e) * p.ld + x0 + c;
-                double v = *gp;
-                const double *pe = panel + e * bs;
-                if (MODE == MODE_ROW) {
-                    for (int ls = 0; ls < bw; ++ls)
-                        v = __dsub_rn(v, __dmul_rn(pe[ls], Ach[ls * kLuXC + c]));
-                } else {
-                    for (int ls = 0; ls < bw; ++ls)
-                        v = __dsub_rn(v, __dmul_rn(Ach[ls * kLuXC + c], pe[ls]));
+            // rows by warp (kLuRPW per pass, all loads in flight first),
+            // columns by lane (up to two per lane): coalesced, division-free
+            {
+                const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+                const bool c0ok = lane < xc, c1ok = lane + 32 < xc;
+                for (int eb = warp * kLuRPW; eb < ne; eb += nwarp * kLuRPW) {
+                    double v[kLuRPW][2];
+                    bool live[kLuRPW];
+#pragma unroll
+                    for (int r = 0; r < kLuRPW; ++r) {
+                        const int e = eb + r;
+                        live[r] = e < ne && pos[e] >= J + bw;  // pivots are frozen
+                        const double *gp = p.w + (e0 + e) * p.ld + x0 + lane;
+                        v[r][0] = live[r] && c0ok ? gp[0] : 0.0;
+                        v[r][1] = live[r] && c1ok ? gp[32] : 0.0;
+                    }
+#pragma unroll
+                    for (int r = 0; r < kLuRPW; ++r) {
+                        if (!live[r]) continue;
+                        const double *pe = panel + (eb + r) * bs;
+                        for (int ls = 0; ls < bw; ++ls) {
+                            const double pv = pe[ls];
+                            const double a0 = Ach[ls * kLuXC + lane];
+                            const double a1 = Ach[ls * kLuXC + (lane + 32 < kLuXC ? lane + 32 : lane)];
+                            if (MODE == MODE_ROW) {
+                                v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
+                                v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
+                            } else {
+                                v[r][0] = __dsub_rn(v[r][0], __dmul_rn(a0, pv));
+                                v[r][1] = __dsub_rn(v[r][1], __dmul_rn(a1, pv));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < kLuRPW; ++r) {
+                        if (!live[r]) continue;
+                        double *gp = p.w + (e0 + eb + r) * p.ld + x0 + lane;
+                        if (c0ok) gp[0] = v[r][0];
+                        if (c1ok) gp[32] = v[r][1];
+                    }
                 }
-                *gp = v;
             }
             __syncthreads();
         }
