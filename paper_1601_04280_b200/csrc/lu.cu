@@ -178,10 +178,30 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
 
     for (int J = 0; J < k; J += b) {
         const int bw = min(b, k - J);  // this panel's width
-        // load panel columns [J, J+bw) of own entities
-        for (int w = tid; w < ne * bw; w += blockDim.x) {
-            int e = w / bw, x = w % bw;
-            panel[e * bs + x] = p.w[(e0 + e) * p.ld + J + x];
+        // load panel columns [J, J+bw) of own entities: lanes over (row,
+        // column) pairs, 4 row groups of loads in flight per warp
+        {
+            const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+            const int bwl = bw < 32 ? bw : 32;
+            const int rpl = 32 / bwl, r = lane / bwl, xl = lane - r * bwl;
+            const int step = nwarp * rpl;
+            for (int xb = 0; xb < bw; xb += bwl) {
+                const int x = xb + xl;
+                const bool xok = r < rpl && x < bw;
+                for (int eb = warp * rpl; eb < ne; eb += 4 * step) {
+                    double v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = eb + u * step + r;
+                        v[u] = xok && e < ne ? p.w[(e0 + e) * p.ld + J + x] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = eb + u * step + r;
+                        if (xok && e < ne) panel[e * bs + x] = v[u];
+                    }
+                }
+            }
         }
         __syncthreads();
 
@@ -284,19 +304,32 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
         }
 
         // write the panel back
-        for (int w = tid; w < ne * bw; w += blockDim.x) {
-            int e = w / bw, x = w % bw;
-            p.w[(e0 + e) * p.ld + J + x] = panel[e * bs + x];
+        {
+            const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+            const int bwl = bw < 32 ? bw : 32;
+            const int rpl = 32 / bwl, r = lane / bwl, xl = lane - r * bwl;
+            for (int xb = 0; xb < bw; xb += bwl) {
+                const int x = xb + xl;
+                if (r >= rpl || x >= bw) continue;
+                for (int e = warp * rpl + r; e < ne; e += nwarp * rpl)
+                    p.w[(e0 + e) * p.ld + J + x] = panel[e * bs + x];
+            }
         }
 
         // deferred trailing update of columns [J+bw, k)
         for (int x0 = J + bw; x0 < k; x0 += kLuXC) {
             const int xc = min(kLuXC, k - x0);
-            // A_s[x] for the panel's pivots (tiny triangular recurrence)
+            // A_s[x] for the panel's pivots (tiny triangular recurrence); the
+            // pivot rows' values are first staged (all loads in flight)
+            for (int w = tid; w < bw * xc; w += blockDim.x) {
+                const int ls = w / xc, c = w - ls * xc;
+                Ach[ls * kLuXC + c] = __ldcg(p.w + (int64_t)pw_ent[ls] * p.ld + x0 + c);
+            }
+            __syncthreads();
             for (int c = tid; c < xc; c += blockDim.x) {
                 const int x = x0 + c;
                 for (int ls = 0; ls < bw; ++ls) {
-                    double v = __ldcg(p.w + (int64_t)pw_ent[ls] * p.ld + x);
+                    double v = Ach[ls * kLuXC + c];
                     const double *pr = PR + ls * b;
                     if (MODE == MODE_ROW) {
                         for (int l2 = 0; l2 < ls; ++l2)
@@ -312,22 +345,38 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 }
             }
             __syncthreads();
-            // rows by warp (kLuRPW per pass, all loads in flight first),
-            // columns by lane (up to two per lane): coalesced, division-free
+            // rows by warp (kLuRPW per pass), columns by lane (up to two per
+            // lane): coalesced, division-free; the next pass's loads are
+            // issued before this pass's arithmetic (software pipeline)
             {
                 const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
                 const bool c0ok = lane < xc, c1ok = lane + 32 < xc;
-                for (int eb = warp * kLuRPW; eb < ne; eb += nwarp * kLuRPW) {
+                const int a1i = lane + 32 < kLuXC ? lane + 32 : lane;
+                const int stride = nwarp * kLuRPW;
+                double vn[kLuRPW][2];
+                bool ln[kLuRPW];
+                auto fetch = [&](int eb) {
+#pragma unroll
+                    for (int r = 0; r < kLuRPW; ++r) {
+                        const int e = eb + r;
+                        ln[r] = e < ne && pos[e] >= J + bw;  // pivots are frozen
+                        const double *gp = p.w + (e0 + e) * p.ld + x0 + lane;
+                        vn[r][0] = ln[r] && c0ok ? gp[0] : 0.0;
+                        vn[r][1] = ln[r] && c1ok ? gp[32] : 0.0;
+                    }
+                };
+                int eb = warp * kLuRPW;
+                if (eb < ne) fetch(eb);
+                for (; eb < ne; eb += stride) {
                     double v[kLuRPW][2];
                     bool live[kLuRPW];
 #pragma unroll
                     for (int r = 0; r < kLuRPW; ++r) {
-                        const int e = eb + r;
-                        live[r] = e < ne && pos[e] >= J + bw;  // pivots are frozen
-                        const double *gp = p.w + (e0 + e) * p.ld + x0 + lane;
-                        v[r][0] = live[r] && c0ok ? gp[0] : 0.0;
-                        v[r][1] = live[r] && c1ok ? gp[32] : 0.0;
+                        v[r][0] = vn[r][0];
+                        v[r][1] = vn[r][1];
+                        live[r] = ln[r];
                     }
+                    if (eb + stride < ne) fetch(eb + stride);
 #pragma unroll
                     for (int r = 0; r < kLuRPW; ++r) {
                         if (!live[r]) continue;
@@ -335,7 +384,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                         for (int ls = 0; ls < bw; ++ls) {
                             const double pv = pe[ls];
                             const double a0 = Ach[ls * kLuXC + lane];
-                            const double a1 = Ach[ls * kLuXC + (lane + 32 < kLuXC ? lane + 32 : lane)];
+                            const double a1 = Ach[ls * kLuXC + a1i];
                             if (MODE == MODE_ROW) {
                                 v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
                                 v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
@@ -361,8 +410,9 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     // ---- final assembly (after everyone's write-backs and CTA 0's piv rows)
     bar_target += G;
     grid_arrive_wait(p.bar, bar_target);
-    for (int w = tid; w < ne * k; w += blockDim.x) {
-        const int e = w / k, x = w % k;
+    const int lane_f = tid & 31, warp_f = tid >> 5, nwarp_f = blockDim.x >> 5;
+    for (int e = warp_f; e < ne; e += nwarp_f)
+    for (int x = lane_f; x < k; x += 32) {
         const int q = pos[e];
         double v;
         if (q < k) {
