@@ -1741,26 +1741,37 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
 #pragma unroll
                     for (int ls = 0; ls < B; ++ls)
                         l[ls] = ls < bw ? __ldcg(wt + (int64_t)(J + ls) * ldt + e) : 0.0;
-                    // columns 4*grp + {0..3} + 4*ngrp*it: four independent loads
-                    // in flight per thread
-                    for (int c0 = 4 * grp; c0 < tw; c0 += 4 * ngrp) {
-                        double v[4];
+                    // columns 4*grp + {0..3} + 4*ngrp*it, three such groups
+                    // (twelve independent loads) in flight per thread
+                    constexpr int NI = 3;
+                    for (int cb = 4 * grp; cb < tw; cb += NI * 4 * ngrp) {
+                        double v[NI][4];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            v[i] = c0 + i < tw ? __ldcg(wt + (int64_t)(x0 + c0 + i) * ldt + e) : 0.0;
+                        for (int q = 0; q < NI; ++q)
 #pragma unroll
-                        for (int ls = 0; ls < B; ++ls)
-                            if (ls < bw) {
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const double av = Ach[ls * AW + c0 + i];  // zero past tw
-                                    v[i] = MODE == MODE_ROW ? __dsub_rn(v[i], __dmul_rn(l[ls], av))
-                                                            : __dsub_rn(v[i], __dmul_rn(av, l[ls]));
-                                }
+                            for (int i = 0; i < 4; ++i) {
+                                const int c = cb + q * 4 * ngrp + i;
+                                v[q][i] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + e) : 0.0;
                             }
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            if (c0 + i < tw) wt[(int64_t)(x0 + c0 + i) * ldt + e] = v[i];
+                        for (int q = 0; q < NI; ++q) {
+                            const int c0 = cb + q * 4 * ngrp;
+                            if (c0 >= tw) break;
+#pragma unroll
+                            for (int ls = 0; ls < B; ++ls)
+                                if (ls < bw) {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        const double av = Ach[ls * AW + c0 + i];  // zero past tw
+                                        v[q][i] = MODE == MODE_ROW
+                                                      ? __dsub_rn(v[q][i], __dmul_rn(l[ls], av))
+                                                      : __dsub_rn(v[q][i], __dmul_rn(av, l[ls]));
+                                    }
+                                }
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                if (c0 + i < tw) wt[(int64_t)(x0 + c0 + i) * ldt + e] = v[q][i];
+                        }
                     }
                 }
             }
@@ -1952,8 +1963,11 @@ static int try_run_lu_hybrid(LuParams prm, void *ws, cudaStream_t stream) {
         if (atoi(env)) return 1;
     if (prm.M > kLuClusterMaxM || prm.k > 1024) return 1;
     bool launched = false;
-    const int rc = prm.k <= 8 ? try_run_lu_hybrid_b<MODE, 8, 2>(prm, ws, stream, &launched)
-                              : try_run_lu_hybrid_b<MODE, 12, 2>(prm, ws, stream, &launched);
+    const int hb = getenv("SRLU_LU_HYBRID_B") ? atoi(getenv("SRLU_LU_HYBRID_B")) : 0;  // testing knob
+    // B = 8 measured faster than 12 at BASELINE config 2 (smaller per-step
+    // code: the step is specialised per in-panel index)
+    const int rc = hb != 12 ? try_run_lu_hybrid_b<MODE, 8, 2>(prm, ws, stream, &launched)
+                            : try_run_lu_hybrid_b<MODE, 12, 2>(prm, ws, stream, &launched);
     if (rc != SRLU_OK) return rc;
     return launched ? SRLU_OK : 1;
 }

@@ -37,8 +37,8 @@ int main(int argc, char **argv) {
         cudaEventElapsedTime(&ms, e0, e1);
         long long t[8];
         cudaMemcpyFromSymbol(t, g_lu_trace, sizeof(t));
-        printf("rc=%d %.1f us | winner %lld bookkeep %lld argmax+push %lld phases %lld wait %lld first %lld rest %lld"
-               " (cycles, rank 0)  %s\n", rc, ms * 1e3, t[0], t[1], t[2], t[3], t[4], t[5], t[6],
+        printf("rc=%d %.1f us | t0 %lld t1 %lld t2 %lld t3 %lld t4 %lld t5 %lld t6 %lld t7 %lld"
+               " (cycles, rank 0)  %s\n", rc, ms * 1e3, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7],
                cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
