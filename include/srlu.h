@@ -78,6 +78,14 @@ int srlu_build_composite(uint64_t seed, int64_t k, int64_t l, int64_t n, int32_t
                          int32_t *sample_idx, int64_t *pad, void *staging, size_t staging_bytes,
                          void *ws, size_t ws_bytes, srlu_stream_t stream);
 
+/* build_composite plus, when sched != NULL, the scheduled K1's gather
+ * schedule for an A of element type dtype (srlu_k1_schedule), in one call. */
+int srlu_build_composite_k1(uint64_t seed, int64_t k, int64_t l, int64_t n, int32_t *row_of,
+                            double *sign, int32_t *sorted, int32_t *bucket_ptr, double *phase,
+                            int32_t *sample_idx, int64_t *pad, void *staging, size_t staging_bytes,
+                            void *ws, size_t ws_bytes, int dtype, void *sched, size_t sched_bytes,
+                            srlu_stream_t stream);
+
 /* build_sem(l, n, seed) on the DEVICE: row_of[n] in [0,l), sign[n] = +-1.
  * Bit-exact with numpy Generator(Philox(seed)).integers (Lemire). */
 size_t srlu_draw_sem_workspace(int64_t n, int64_t l);

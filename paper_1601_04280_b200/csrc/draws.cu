@@ -276,20 +276,40 @@ extern "C" int srlu_build_composite(uint64_t seed, int64_t k, int64_t l, int64_t
     SRLU_REQUIRE(ws_bytes >= srlu_build_composite_workspace(n, l), SRLU_ERR_WORKSPACE,
                  "build_composite: workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
+    // device work first (the GPU starts while the host draws the transform)
+    char *w = (char *)ws;
+    const size_t ws_sem = align256(srlu_draw_sem_workspace(n, l));
+    int rc = srlu_draw_sem(seed, l, n, row_of, sign, w, ws_sem, stream);
+    if (rc != SRLU_OK) return rc;
+    rc = srlu_sem_plan(row_of, sign, n, l, sorted, bucket_ptr, w + ws_sem, ws_bytes - ws_sem,
+                       stream);
+    if (rc != SRLU_OK) return rc;
     double *ph = (double *)staging;
     int64_t *idx64 = (int64_t *)(ph + l);
     int32_t *idx32 = (int32_t *)(idx64 + k);
     // transform stage: seed + 2**32 (sketch.py:36, :276)
-    int rc = srlu_draw_fast_transform(seed + (1ULL << 32), k, l, ph, idx64, pad);
+    rc = srlu_draw_fast_transform(seed + (1ULL << 32), k, l, ph, idx64, pad);
     if (rc != SRLU_OK) return rc;
     for (int64_t i = 0; i < k; ++i) idx32[i] = (int32_t)idx64[i];
     SRLU_CUDA(cudaMemcpyAsync(phase, ph, sizeof(double) * (size_t)l, cudaMemcpyHostToDevice, s));
     SRLU_CUDA(cudaMemcpyAsync(sample_idx, idx32, sizeof(int32_t) * (size_t)k,
                               cudaMemcpyHostToDevice, s));
-    char *w = (char *)ws;
-    const size_t ws_sem = align256(srlu_draw_sem_workspace(n, l));
-    rc = srlu_draw_sem(seed, l, n, row_of, sign, w, ws_sem, stream);
-    if (rc != SRLU_OK) return rc;
-    return srlu_sem_plan(row_of, sign, n, l, sorted, bucket_ptr, w + ws_sem, ws_bytes - ws_sem,
-                         stream);
+    return SRLU_OK;
+}
+
+extern "C" size_t srlu_k1_schedule_bytes(int64_t n, int64_t l1, int64_t pad1, int dtype);
+extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bucket_ptr1, int64_t n,
+                                int64_t l1, int64_t pad1, int dtype, void *sched,
+                                size_t sched_bytes, srlu_stream_t stream);
+
+extern "C" int srlu_build_composite_k1(uint64_t seed, int64_t k, int64_t l, int64_t n,
+                                       int32_t *row_of, double *sign, int32_t *sorted,
+                                       int32_t *bucket_ptr, double *phase, int32_t *sample_idx,
+                                       int64_t *pad, void *staging, size_t staging_bytes, void *ws,
+                                       size_t ws_bytes, int dtype, void *sched, size_t sched_bytes,
+                                       srlu_stream_t stream) {
+    int rc = srlu_build_composite(seed, k, l, n, row_of, sign, sorted, bucket_ptr, phase,
+                                  sample_idx, pad, staging, staging_bytes, ws, ws_bytes, stream);
+    if (rc != SRLU_OK || sched == nullptr) return rc;
+    return srlu_k1_schedule(sorted, bucket_ptr, n, l, *pad, dtype, sched, sched_bytes, stream);
 }

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import logging
 import math
+import threading
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -28,6 +29,7 @@ import torch
 from .errors import DecompositionError, ParameterError, ShapeError, SingularMatrixError
 from .factor import check_rank, dgemm, lu_col_pivot_dev, lu_row_pivot_dev, pinv_dev
 from .matrix import COMPLEX, REAL, Matrix, Permutation
+from . import _lib
 from .sketch import (HADAMARD, build_composite, members, sketch_left_into, sketch_right_into,
                      transform_kind_for_field)
 
@@ -194,6 +196,23 @@ def _pipeline(a: Matrix, params: RandLuParams, keep: bool) -> RandLuResult:
 _SIDE_STREAMS = {}
 
 
+_EVENTS = threading.local()
+
+
+def _stage_events(dev, n):
+    """Timing events of an attempt, created once per (thread, device) and
+    re-recorded (their elapsed times are read before the attempt returns)."""
+    key = torch.device(dev).index
+    pool = getattr(_EVENTS, "pool", None)
+    if pool is None:
+        pool = _EVENTS.pool = {}
+    evs = pool.get(key)
+    if evs is None or len(evs) < n:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        pool[key] = evs
+    return evs[:n]
+
+
 def _side_stream(dev):
     key = torch.device(dev).index
     if key not in _SIDE_STREAMS:
@@ -217,10 +236,12 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     kind = transform_kind_for_field(params.field)
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
+    ev = _stage_events(dev, len(STAGES) + 1)
     ev[0].record(main)
 
-    om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev)
+    k1_dtype = None if a.is_sparse else _lib.dtype_code(a.raw.dtype)
+    om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev,
+                          k1_dtype=k1_dtype)
     y = torch.empty(m, k1, dtype=torch.float64, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     sketch_right_into(a, om1, y, flag)

@@ -226,10 +226,39 @@ class _StagingPool:
 _STAGING = _StagingPool()
 
 
-def build_composite(k, l, n, kind, seed, device=None, stream=None) -> CompositeSketch:
+_LAYOUTS = {}
+
+
+def _composite_layout(L, k, l, n, k1_dtype):
+    """Byte layout of one composite sketch (+ optional K1 schedule) in a
+    single device buffer; cached per shape."""
+    key = (k, l, n, k1_dtype)
+    lay = _LAYOUTS.get(key)
+    if lay is None:
+        i4 = lambda c: ((c * 4 + 7) // 8) * 8
+        off = {"sign": 0, "phase": n * 8}
+        off["row"] = off["phase"] + l * 8
+        off["sorted"] = off["row"] + i4(n)
+        off["bptr"] = off["sorted"] + i4(n)
+        off["idx"] = off["bptr"] + i4(l + 1)
+        off["ws"] = ((off["idx"] + i4(k)) + 255) // 256 * 256
+        ws_bytes = L.srlu_build_composite_workspace(n, l)
+        sched_bytes = 0
+        if k1_dtype is not None:
+            sched_bytes = L.srlu_k1_schedule_bytes(n, l, _next_pow2(l), k1_dtype)
+        off["sched"] = (off["ws"] + ws_bytes + 255) // 256 * 256
+        total = off["sched"] + max(sched_bytes, 0)
+        lay = (off, ws_bytes, sched_bytes, total, L.srlu_build_composite_staging(k, l))
+        _LAYOUTS[key] = lay
+    return lay
+
+
+def build_composite(k, l, n, kind, seed, device=None, stream=None, k1_dtype=None) -> CompositeSketch:
     """sketch.py:269-278 (transform stage seeded seed + 2**32), in one C-ABI
-    call: host transform draws -> pinned staging -> upload, device sparse
-    draws and the accumulation plan, all enqueued on `stream`."""
+    call: device sparse draws and the accumulation plan, then host transform
+    draws -> pinned staging -> upload, all enqueued on `stream`; with
+    ``k1_dtype`` (an A element-type code) also the scheduled K1's gather
+    schedule.  The device work is enqueued before the Python bookkeeping."""
     if kind not in (FOURIER, HADAMARD):
         raise ParameterError(f"unknown transform kind {kind!r}")
     if kind == FOURIER:
@@ -242,38 +271,32 @@ def build_composite(k, l, n, kind, seed, device=None, stream=None) -> CompositeS
     seed = _check_seed(seed)
     L = _lib.lib()
     dev = torch.device(device) if device is not None else _default_device()
-    # one device allocation carved into the sketch's arrays (8-byte arrays first)
-    n8, l8 = n * 8, l * 8
-    i4 = lambda c: ((c * 4 + 7) // 8) * 8
-    off_sign, off_phase = 0, n8
-    off_row = off_phase + l8
-    off_sorted = off_row + i4(n)
-    off_bptr = off_sorted + i4(n)
-    off_idx = off_bptr + i4(l + 1)
-    off_ws = ((off_idx + i4(k)) + 255) // 256 * 256
-    ws_bytes = L.srlu_build_composite_workspace(n, l)
-    buf = torch.empty(off_ws + ws_bytes, dtype=torch.uint8, device=dev)
-    isz = {torch.float64: 8, torch.int32: 4}
-    view = lambda off, cnt, dt: buf[off:off + cnt * isz[dt]].view(dt)
-    sign = view(off_sign, n, torch.float64)
-    phase = view(off_phase, l, torch.float64)
-    row_of = view(off_row, n, torch.int32)
-    srt = view(off_sorted, n, torch.int32)
-    bptr = view(off_bptr, l + 1, torch.int32)
-    idx = view(off_idx, k, torch.int32)
-    st_bytes = L.srlu_build_composite_staging(k, l)
+    off, ws_bytes, sched_bytes, total, st_bytes = _composite_layout(L, k, l, n, k1_dtype)
+    buf = torch.empty(total, dtype=torch.uint8, device=dev)
+    base = buf.data_ptr()
     staging = _STAGING.get(st_bytes)
     padc = ctypes.c_int64(0)
     sh = _lib.stream_handle(stream)
-    _lib.check(L.srlu_build_composite(seed, k, l, n, _lib.ptr(row_of), _lib.ptr(sign),
-                                      _lib.ptr(srt), _lib.ptr(bptr), _lib.ptr(phase), _lib.ptr(idx),
-                                      ctypes.addressof(padc), staging.data_ptr(), staging.numel(),
-                                      buf.data_ptr() + off_ws, ws_bytes, sh), "build_composite")
+    P_ = ctypes.c_void_p
+    _lib.check(L.srlu_build_composite_k1(
+        seed, k, l, n, P_(base + off["row"]), P_(base + off["sign"]), P_(base + off["sorted"]),
+        P_(base + off["bptr"]), P_(base + off["phase"]), P_(base + off["idx"]),
+        ctypes.addressof(padc), staging.data_ptr(), staging.numel(), P_(base + off["ws"]),
+        ws_bytes, -1 if k1_dtype is None else k1_dtype,
+        P_(base + off["sched"]) if sched_bytes else None, sched_bytes, sh),
+        "build_composite_k1" if sched_bytes else "build_composite")
     _STAGING.put(staging, stream if stream is not None else torch.cuda.current_stream(dev))
     assert padc.value == pad
-    sem = SparseEmbedding(int(l), int(n), row_of, sign, seed=seed)
-    sem._plan.extend([srt, bptr])
-    fast = FastTransformSketch(int(k), int(l), phase, idx, pad, math.sqrt(pad / k), kind,
+    isz = {torch.float64: 8, torch.int32: 4}
+    view = lambda o, cnt, dt: buf[off[o]:off[o] + cnt * isz[dt]].view(dt)
+    sem = SparseEmbedding(int(l), int(n), view("row", n, torch.int32),
+                          view("sign", n, torch.float64), seed=seed)
+    sem._plan.extend([view("sorted", n, torch.int32), view("bptr", l + 1, torch.int32)])
+    if k1_dtype is not None:
+        sem._sched.append((("k1s", k1_dtype, pad),
+                           buf[off["sched"]:off["sched"] + sched_bytes] if sched_bytes else None))
+    fast = FastTransformSketch(int(k), int(l), view("phase", l, torch.float64),
+                               view("idx", k, torch.int32), pad, math.sqrt(pad / k), kind,
                                seed=seed + STAGE_SEED_OFFSET)
     return CompositeSketch(sem, fast)
 

@@ -24,10 +24,10 @@ for it in range(8):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     h0 = time.perf_counter()
     ev[0].record()
-    om = build_composite(prm["k1"], prm["l1"], cfg["n"], "hadamard", it, "cuda")
+    om = build_composite(prm["k1"], prm["l1"], cfg["n"], "hadamard", it, "cuda",
+                         k1_dtype=None if A.is_sparse else P._lib.dtype_code(A.raw.dtype))
     h1 = time.perf_counter()
     ev[1].record()
-    om.sem.k1_schedule(P._lib.dtype_code(A.raw.dtype), om.fast.pad) if not A.is_sparse else None
     h2 = time.perf_counter()
     ev[2].record()
     sketch_right_into(A, om, y, flag)
@@ -37,5 +37,5 @@ for it in range(8):
     rows.append([(h1 - h0) * 1e3, (h2 - h1) * 1e3, (h3 - h2) * 1e3,
                  ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
 r = np.median(np.array(rows[2:]), axis=0)
-print(f"config {c}: host ms composite {r[0]:.3f} sched {r[1]:.3f} k1-call {r[2]:.3f} | "
+print(f"config {c}: host ms composite+sched {r[0]:.3f} - {r[1]:.3f} k1-call {r[2]:.3f} | "
       f"gpu ms composite {r[3]:.3f} sched {r[4]:.3f} k1 {r[5]:.3f}")
