@@ -68,7 +68,7 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
                                 const int32_t *__restrict__ row_of2,
                                 const double *__restrict__ sign2,
                                 const int64_t *__restrict__ colptr, int *__restrict__ fill,
-                                unsigned long long *__restrict__ keys, double *__restrict__ ev) {
+                                ulonglong2 *__restrict__ ent) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -81,8 +81,7 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
             const int j = indices[p];
             const int64_t slot = colptr[j] + atomicAdd(fill + j, 1);
             const double v = (double)vals[p];
-            keys[slot] = key;
-            ev[slot] = neg ? -v : v;
+            ent[slot] = make_ulonglong2(key, (unsigned long long)__double_as_longlong(neg ? -v : v));
         }
     }
 }
@@ -90,10 +89,9 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
 // One CTA per column (grid-stride); handles columns with lo < count <= CAP.
 template <int CAP>
 __global__ void __launch_bounds__(256) csr_col_project_kernel(
-    const int64_t *__restrict__ colptr, const unsigned long long *__restrict__ keys,
-    const double *__restrict__ ev, int64_t n, int l, int pad, const double *__restrict__ phase,
-    const int32_t *__restrict__ idx, int k, double mult, double *__restrict__ out, int64_t ldo,
-    int *flags, int lo) {
+    const int64_t *__restrict__ colptr, const ulonglong2 *__restrict__ ent, int64_t n, int l,
+    int pad, const double *__restrict__ phase, const int32_t *__restrict__ idx, int k,
+    double mult, double *__restrict__ out, int64_t ldo, int *flags, int lo) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *x = reinterpret_cast<double *>(smem_raw);                          // pad
     unsigned long long *sk = reinterpret_cast<unsigned long long *>(x + pad);  // CAP
@@ -116,8 +114,9 @@ __global__ void __launch_bounds__(256) csr_col_project_kernel(
         while (n2 < cnt) n2 <<= 1;
         for (int i = threadIdx.x; i < n2; i += blockDim.x) {
             if (i < cnt) {
-                sk[i] = keys[p0 + i];
-                sv[i] = ev[p0 + i];
+                const ulonglong2 e = ent[p0 + i];
+                sk[i] = e.x;
+                sv[i] = __longlong_as_double((long long)e.y);
             } else {
                 sk[i] = ~0ULL;
                 sv[i] = 0.0;
@@ -167,11 +166,125 @@ __global__ void __launch_bounds__(256) csr_col_project_kernel(
     }
 }
 
+// One CTA per column (grid-stride) for columns with at most CAP entries
+// (the common case: ~nnz/n entries per column).  The segment is ordered by
+// a counting sort on the bucket t in shared memory (histogram + block scan +
+// scatter); the few entries of one bucket (~nnz/(n*l) on average) are then
+// put in ascending q by the thread that folds that bucket (insertion sort),
+// so every bucket sum is the reference's sequential sum in PA-row order.
+template <int CAP, int NT>
+__global__ void __launch_bounds__(NT) csr_col_bucket_kernel(
+    const int64_t *__restrict__ colptr, const ulonglong2 *__restrict__ ent, int64_t n, int l,
+    int pad, const double *__restrict__ phase, const int32_t *__restrict__ idx, int k,
+    double mult, double *__restrict__ out, int64_t ldo) {
+    constexpr int PER = CAP / NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *x = reinterpret_cast<double *>(smem_raw);   // pad
+    double *sv = x + pad;                               // CAP
+    int *sq = reinterpret_cast<int *>(sv + CAP);         // CAP
+    int *base = sq + CAP;                               // l + 1
+    __shared__ int wsum[NT / 32];
+    const bool reg = pad >= 32;
+    const int bsize = pad < 512 ? pad : 512;
+    const int nb = pad / bsize;
+    const int nzb = (l + bsize - 1) / bsize;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int chunk = (l + NT - 1) / NT;
+    for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+        const int64_t p0 = colptr[j];
+        const int cnt = (int)(colptr[j + 1] - p0);
+        if (cnt > CAP) continue;  // uniform: the bitonic launch takes it
+        for (int t = threadIdx.x; t <= l; t += NT) base[t] = 0;
+        __syncthreads();
+        unsigned long long ek[PER];
+        double evv[PER];
+        int off[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int e = threadIdx.x + r * NT;
+            off[r] = -1;
+            ek[r] = 0;
+            evv[r] = 0.0;
+            if (e < cnt) {
+                const ulonglong2 v = ent[p0 + e];
+                ek[r] = v.x;
+                evv[r] = __longlong_as_double((long long)v.y);
+                off[r] = atomicAdd(base + (int)(v.x >> 32), 1);
+            }
+        }
+        __syncthreads();
+        // exclusive scan of the l bucket counts (chunk per thread)
+        const int c0 = threadIdx.x * chunk;
+        int s = 0;
+        for (int c = 0; c < chunk; ++c)
+            if (c0 + c < l) s += base[c0 + c];
+        int incl = s;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += wsum[w];
+        int run = wpre + incl - s;
+        for (int c = 0; c < chunk; ++c)
+            if (c0 + c < l) {
+                const int v = base[c0 + c];
+                base[c0 + c] = run;
+                run += v;
+            }
+        if (threadIdx.x == NT - 1) base[l] = cnt;
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < PER; ++r)
+            if (off[r] >= 0) {
+                const int pos = base[(int)(ek[r] >> 32)] + off[r];
+                sq[pos] = (int)(unsigned)ek[r];
+                sv[pos] = evv[r];
+            }
+        __syncthreads();
+        for (int t = threadIdx.x; t < pad; t += NT) {
+            double acc = 0.0;
+            if (t < l) {
+                const int b0 = base[t], b1 = base[t + 1];
+                for (int a = b0 + 1; a < b1; ++a) {  // insertion sort by q (tiny runs)
+                    const int qa = sq[a];
+                    const double va = sv[a];
+                    int b = a - 1;
+                    while (b >= b0 && sq[b] > qa) {
+                        sq[b + 1] = sq[b];
+                        sv[b + 1] = sv[b];
+                        --b;
+                    }
+                    sq[b + 1] = qa;
+                    sv[b + 1] = va;
+                }
+                for (int a = b0; a < b1; ++a) acc = __dadd_rn(acc, sv[a]);
+                if (phase[t] < 0.0) acc = -acc;
+            }
+            x[reg ? fwht_sw(t) : t] = acc;
+        }
+        __syncthreads();
+        if (reg) {
+            for (int b = warp; b < nzb; b += NT >> 5) fwht_block_warp_dyn512(x + b * bsize, bsize, lane);
+            __syncthreads();
+        } else {
+            fwht_smem_cta(x, pad);
+        }
+        for (int kk = threadIdx.x; kk < k; kk += NT) {
+            const double fv = reg ? fwht_combine_blocks(x, bsize, nb, idx[kk]) : x[idx[kk]];
+            out[j * ldo + kk] = __dmul_rn(fv, mult);
+        }
+        __syncthreads();
+    }
+}
+
 struct CsrWs {
     int *cnt, *fill, *maxcnt;
     int64_t *colptr;
-    unsigned long long *keys;
-    double *ev;
+    ulonglong2 *ent;
 };
 
 static size_t csr_ws_layout(int64_t n, int64_t nnz, char *base, CsrWs *w) {
@@ -186,8 +299,7 @@ static size_t csr_ws_layout(int64_t n, int64_t nnz, char *base, CsrWs *w) {
     p = take(sizeof(int) * n);             if (w) w->fill = (int *)p;
     p = take(sizeof(int) * 4);             if (w) w->maxcnt = (int *)p;
     p = take(sizeof(int64_t) * (n + 1));   if (w) w->colptr = (int64_t *)p;
-    p = take(sizeof(unsigned long long) * (nnz > 0 ? nnz : 1)); if (w) w->keys = (unsigned long long *)p;
-    p = take(sizeof(double) * (nnz > 0 ? nnz : 1));             if (w) w->ev = (double *)p;
+    p = take(sizeof(ulonglong2) * (nnz > 0 ? nnz : 1)); if (w) w->ent = (ulonglong2 *)p;
     return off;
 }
 
@@ -212,20 +324,22 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         if (blocks > 148 * 16) blocks = 148 * 16;
         csr_fill_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(indptr, indices, vals, rows, inv_perm,
                                                            row_of2, sign2, w.colptr, w.fill,
-                                                           w.keys, w.ev);
+                                                           w.ent);
         SRLU_CHECK_LAUNCH("csr_fill_kernel");
     }
-    // columns with <= 2048 entries: small smem, high occupancy; longer ones
-    // (<= 8192) in a second launch; longer still -> flags |= 2
+    // columns with <= 2048 entries: bucket counting sort (high occupancy);
+    // longer ones (<= 8192) in a bitonic launch; longer still -> flags |= 2
     const int64_t grid = n < 148 * 16 ? n : 148 * 16;
     {
-        size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * 2048;
-        SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel<2048>,
+        constexpr int CAP = 2048, NT = 256;
+        size_t smem = sizeof(double) * pad2 + (sizeof(double) + sizeof(int)) * CAP +
+                      sizeof(int) * (l2 + 1);
+        SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left_csr: pad2 too large");
+        SRLU_CUDA(cudaFuncSetAttribute(csr_col_bucket_kernel<CAP, NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        csr_col_project_kernel<2048><<<(unsigned)grid, 256, smem, s>>>(
-            w.colptr, w.keys, w.ev, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
-            nullptr, -1);
-        SRLU_CHECK_LAUNCH("csr_col_project_kernel<2048>");
+        csr_col_bucket_kernel<CAP, NT><<<(unsigned)grid, NT, smem, s>>>(
+            w.colptr, w.ent, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo);
+        SRLU_CHECK_LAUNCH("csr_col_bucket_kernel");
     }
     {
         size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * kCsrColCap;
@@ -233,7 +347,7 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel<kCsrColCap>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         csr_col_project_kernel<kCsrColCap><<<(unsigned)(grid < 148 ? grid : 148), 256, smem, s>>>(
-            w.colptr, w.keys, w.ev, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
+            w.colptr, w.ent, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
             flags, 2048);
     }
     SRLU_CHECK_LAUNCH("csr_col_project_kernel");

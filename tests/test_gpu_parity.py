@@ -336,3 +336,20 @@ def test_csr_long_columns_bit_exact(P):
     np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
     np.testing.assert_array_equal(res.P.indices, ref["P"])
     np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
+
+
+def test_csr_crowded_buckets_bit_exact(P):
+    """Few stage-2 buckets, ~1600 entries per column: long same-bucket runs whose
+    fold order (ascending PA row) matters; values span many binades."""
+    from scipy.sparse import csr_array
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(77))
+    m, n = 20000, 64
+    d = g.standard_normal((m, n)) * np.exp2(g.integers(-30, 30, size=(m, n)))
+    d[g.random((m, n)) < 0.92] = 0.0
+    prm = dict(r=4, k1=8, l1=40, k2=12, l2=24, seed=3)
+    res = P.sparse_randomized_lu(P.Matrix.sparse(csr_array(d)), P.RandLuParams(**prm), keep=True)
+    ref = O.sparse_randomized_lu(csr_array(d), prm, keep=True)
+    np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
+    np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
