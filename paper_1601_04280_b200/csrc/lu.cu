@@ -83,6 +83,8 @@ struct LuParams {
     Cand *cand;       // [2][G]
     double *candrow;  // [2][G][k]
     double *piv;      // [k][k] trailing parts of pivot entities
+    double *gpanel;   // GB > 0: attribute-major panel [GB][ldp] (L2-resident)
+    int64_t ldp;
 };
 
 __device__ inline bool better(unsigned long long a_abs, unsigned a_pos, unsigned long long b_abs,
@@ -122,7 +124,12 @@ __device__ inline void block_best(unsigned long long &abs, unsigned &pos, int &e
     __syncthreads();
 }
 
-template <int MODE>
+// GB > 0: "L2 panel" variant for tall inputs whose smem panel would be
+// narrow (BASELINE config 4: 7085 entities per CTA leave room for 3 columns):
+// the panel lives in an attribute-major workspace [GB][M] (64 MB at M = 1M:
+// L2-resident, every column access coalesced across threads), with GB-wide
+// register rows and several entities' loads in flight per thread.
+template <int MODE, int GB = 0>
 __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_abs[32];
@@ -133,18 +140,21 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
 
     const int tid = threadIdx.x;
     const int G = gridDim.x;
-    const int k = p.k, b = p.b, bs = p.bs, rpc = p.rpc;
+    const int k = p.k, b = p.b, rpc = p.rpc;
+    const int bs = p.bs;
+    const int64_t es = GB ? 1 : bs, xs = GB ? p.ldp : 1;  // panel[e * es + x * xs]
     const int64_t e0 = (int64_t)blockIdx.x * rpc;
     const int ne = (int)max((int64_t)0, min((int64_t)rpc, p.M - e0));
 
     // smem carve-up
-    double *panel = reinterpret_cast<double *>(smem_raw);          // rpc x bs
-    double *PR = panel + (size_t)rpc * bs;                          // b x b
+    double *const spanel = reinterpret_cast<double *>(smem_raw);   // rpc x bs (GB == 0)
+    double *PR = spanel + (GB ? 0 : (size_t)rpc * bs);              // b x b
     double *u = PR + (size_t)b * b;                                 // b
     double *Ach = u + b;                                            // b x kLuXC
     int *pos = reinterpret_cast<int *>(Ach + (size_t)b * kLuXC);    // rpc
     int *pw_ent = pos + rpc;                                        // b
     unsigned bar_target = 0;
+    LU_T0();
 
     // ---- thresh = PIVOT_RTOL * ||w||_F (deterministic two-level sum) ----
     {
@@ -178,6 +188,8 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
 
     for (int J = 0; J < k; J += b) {
         const int bw = min(b, k - J);  // this panel's width
+        double *const panel = GB ? p.gpanel + e0 : spanel;
+        LU_T(7);
         // load panel columns [J, J+bw) of own entities: lanes over (row,
         // column) pairs, 4 row groups of loads in flight per warp
         {
@@ -198,12 +210,13 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int e = eb + u * step + r;
-                        if (xok && e < ne) panel[e * bs + x] = v[u];
+                        if (xok && e < ne) panel[e * es + x * xs] = v[u];
                     }
                 }
             }
         }
         __syncthreads();
+        LU_T(3);
 
         for (int ls = 0; ls < bw; ++ls) {
             const int s = J + ls;
@@ -212,16 +225,38 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
             unsigned long long babs = 0ULL;
             unsigned bpos = 0xFFFFFFFFu;
             int bent = -1;
-            for (int e = tid; e < ne; e += blockDim.x) {
-                if (pos[e] >= s) {
-                    unsigned long long a =
-                        (unsigned long long)__double_as_longlong(fabs(panel[e * bs + ls]));
-                    if (better(a, (unsigned)pos[e], babs, bpos)) {
-                        babs = a; bpos = (unsigned)pos[e]; bent = e;
+            if (GB) {  // four entities' loads in flight per thread
+                for (int eb = tid; eb < ne; eb += 4 * kLuThreads) {
+                    double v[4];
+                    int ps[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int e = eb + r * kLuThreads;
+                        ps[r] = e < ne ? pos[e] : -1;
+                        v[r] = ps[r] >= s ? panel[(int64_t)e * es + ls * xs] : 0.0;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const unsigned long long a =
+                            (unsigned long long)__double_as_longlong(fabs(v[r]));
+                        if (ps[r] >= s && better(a, (unsigned)ps[r], babs, bpos)) {
+                            babs = a; bpos = (unsigned)ps[r]; bent = eb + r * kLuThreads;
+                        }
+                    }
+                }
+            } else {
+                for (int e = tid; e < ne; e += blockDim.x) {
+                    if (pos[e] >= s) {
+                        unsigned long long a =
+                            (unsigned long long)__double_as_longlong(fabs(panel[e * bs + ls]));
+                        if (better(a, (unsigned)pos[e], babs, bpos)) {
+                            babs = a; bpos = (unsigned)pos[e]; bent = e;
+                        }
                     }
                 }
             }
             block_best(babs, bpos, bent, s_abs, s_pos, s_ent);
+            LU_T(0);
             // 2. publish
             Cand *cs = p.cand + (size_t)slot * G;
             double *crow = p.candrow + ((size_t)slot * G + blockIdx.x) * k;
@@ -233,10 +268,11 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 cs[blockIdx.x] = c;
             }
             if (bent >= 0)
-                for (int x = tid; x < bw; x += blockDim.x) crow[x] = panel[bent * bs + x];
+                for (int x = tid; x < bw; x += blockDim.x) crow[x] = panel[bent * es + x * xs];
             // 3. one grid barrier per pivot step
             bar_target += G;
             grid_arrive_wait(p.bar, bar_target);
+            LU_T(1);
             // 4. global winner
             {
                 unsigned long long ga = 0ULL;
@@ -258,6 +294,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 }
                 __syncthreads();
             }
+            LU_T(2);
             const int went = pw_ent[ls];
             const int wpos = (int)s_pos[1];
             const double pivv = u[ls];
@@ -271,7 +308,71 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
             }
             __syncthreads();
             // 6. apply the step to own panel columns
-            if (MODE == MODE_ROW) {
+            constexpr int RA = GB <= 8 ? 4 : 2;  // entities in flight (GB > 0)
+            if (GB && MODE == MODE_ROW) {
+                for (int eb = tid; eb < ne; eb += RA * kLuThreads) {
+                    double v[RA][GB > 0 ? GB : 1], lv[RA];
+                    bool act[RA];
+#pragma unroll
+                    for (int r = 0; r < RA; ++r) {
+                        const int e = eb + r * kLuThreads;
+                        act[r] = e < ne && pos[e] > s;
+                        const double *we = panel + (int64_t)e * es;
+                        lv[r] = act[r] ? we[ls * xs] : 0.0;
+#pragma unroll
+                        for (int x = 0; x < GB; ++x)
+                            v[r][x] = (act[r] && big && x > ls && x < bw) ? we[x * xs] : 0.0;
+                    }
+#pragma unroll
+                    for (int r = 0; r < RA; ++r) {
+                        if (!act[r]) continue;
+                        double *we = panel + (int64_t)(eb + r * kLuThreads) * es;
+                        if (big) {
+                            const double l = lv[r] / pivv;
+                            we[ls * xs] = l;
+#pragma unroll
+                            for (int x = 0; x < GB; ++x)
+                                if (x > ls && x < bw) we[x * xs] = __dsub_rn(v[r][x], __dmul_rn(l, u[x]));
+                        } else {
+                            we[ls * xs] = 0.0;
+                        }
+                    }
+                }
+            } else if (GB) {
+                // multipliers of the pivot column: L[x] = u[x] / piv
+                for (int x = ls + 1 + tid; x < bw; x += blockDim.x) u[x] = big ? u[x] / pivv : 0.0;
+                __syncthreads();
+                for (int eb = tid; eb < ne; eb += RA * kLuThreads) {
+                    double v[RA][GB > 0 ? GB : 1], cv[RA];
+                    bool act[RA], isw[RA];
+#pragma unroll
+                    for (int r = 0; r < RA; ++r) {
+                        const int e = eb + r * kLuThreads;
+                        isw[r] = e < ne && e0 + e == went;
+                        act[r] = e < ne && !isw[r] && big && pos[e] > s;
+                        const double *we = panel + (int64_t)e * es;
+                        cv[r] = act[r] ? we[ls * xs] : 0.0;
+#pragma unroll
+                        for (int x = 0; x < GB; ++x)
+                            v[r][x] = (act[r] && x > ls && x < bw) ? we[x * xs] : 0.0;
+                    }
+#pragma unroll
+                    for (int r = 0; r < RA; ++r) {
+                        double *we = panel + (int64_t)(eb + r * kLuThreads) * es;
+                        if (isw[r]) {
+#pragma unroll
+                            for (int x = 0; x < GB; ++x)
+                                if (x > ls && x < bw) we[x * xs] = u[x];
+                        } else if (act[r]) {
+#pragma unroll
+                            for (int x = 0; x < GB; ++x)
+                                if (x > ls && x < bw) we[x * xs] = __dsub_rn(v[r][x], __dmul_rn(u[x], cv[r]));
+                        }
+                    }
+                }
+                if (b < k)
+                    for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
+            } else if (MODE == MODE_ROW) {
                 for (int e = tid; e < ne; e += blockDim.x) {
                     if (pos[e] <= s) continue;
                     double *we = panel + e * bs;
@@ -301,6 +402,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                     for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
             }
             __syncthreads();
+            LU_T(6);
         }
 
         // write the panel back
@@ -312,7 +414,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 const int x = xb + xl;
                 if (r >= rpl || x >= bw) continue;
                 for (int e = warp * rpl + r; e < ne; e += nwarp * rpl)
-                    p.w[(e0 + e) * p.ld + J + x] = panel[e * bs + x];
+                    p.w[(e0 + e) * p.ld + J + x] = panel[e * es + x * xs];
             }
         }
 
@@ -345,41 +447,65 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 }
             }
             __syncthreads();
-            // rows by warp (kLuRPW per pass), columns by lane (up to two per
+            // rows by warp (RPW per pass), columns by lane (up to two per
             // lane): coalesced, division-free; the next pass's loads are
             // issued before this pass's arithmetic (software pipeline)
             {
+                constexpr int RPW = kLuRPW;  // 8 with the L2 panel: spills, measured slower
                 const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
                 const bool c0ok = lane < xc, c1ok = lane + 32 < xc;
                 const int a1i = lane + 32 < kLuXC ? lane + 32 : lane;
-                const int stride = nwarp * kLuRPW;
-                double vn[kLuRPW][2];
-                bool ln[kLuRPW];
+                const int stride = nwarp * RPW;
+                double vn[RPW][2];
+                double pmn[RPW];  // GB: lane x holds multiplier x of row r
+                bool ln[RPW];
                 auto fetch = [&](int eb) {
 #pragma unroll
-                    for (int r = 0; r < kLuRPW; ++r) {
+                    for (int r = 0; r < RPW; ++r) {
                         const int e = eb + r;
                         ln[r] = e < ne && pos[e] >= J + bw;  // pivots are frozen
                         const double *gp = p.w + (e0 + e) * p.ld + x0 + lane;
                         vn[r][0] = ln[r] && c0ok ? gp[0] : 0.0;
                         vn[r][1] = ln[r] && c1ok ? gp[32] : 0.0;
+                        pmn[r] = GB && ln[r] && lane < bw ? panel[(int64_t)e * es + lane * xs] : 0.0;
                     }
                 };
-                int eb = warp * kLuRPW;
+                int eb = warp * RPW;
                 if (eb < ne) fetch(eb);
                 for (; eb < ne; eb += stride) {
-                    double v[kLuRPW][2];
-                    bool live[kLuRPW];
+                    double v[RPW][2];
+                    double pm[RPW];
+                    bool live[RPW];
 #pragma unroll
-                    for (int r = 0; r < kLuRPW; ++r) {
+                    for (int r = 0; r < RPW; ++r) {
                         v[r][0] = vn[r][0];
                         v[r][1] = vn[r][1];
                         live[r] = ln[r];
+                        pm[r] = pmn[r];
                     }
                     if (eb + stride < ne) fetch(eb + stride);
+                    if (GB) {  // all lanes shuffle (stores below are gated by live)
 #pragma unroll
-                    for (int r = 0; r < kLuRPW; ++r) {
-                        if (!live[r]) continue;
+                        for (int ls = 0; ls < (GB > 0 ? GB : 1); ++ls) {
+                            if (ls >= bw) break;
+                            const double a0 = Ach[ls * kLuXC + lane];
+                            const double a1 = Ach[ls * kLuXC + a1i];
+#pragma unroll
+                            for (int r = 0; r < RPW; ++r) {
+                                const double pv = __shfl_sync(0xffffffffu, pm[r], ls);
+                                if (MODE == MODE_ROW) {
+                                    v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
+                                    v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
+                                } else {
+                                    v[r][0] = __dsub_rn(v[r][0], __dmul_rn(a0, pv));
+                                    v[r][1] = __dsub_rn(v[r][1], __dmul_rn(a1, pv));
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r) {
+                        if (!live[r] || GB) continue;
                         const double *pe = panel + (eb + r) * bs;
                         for (int ls = 0; ls < bw; ++ls) {
                             const double pv = pe[ls];
@@ -395,7 +521,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                         }
                     }
 #pragma unroll
-                    for (int r = 0; r < kLuRPW; ++r) {
+                    for (int r = 0; r < RPW; ++r) {
                         if (!live[r]) continue;
                         double *gp = p.w + (e0 + eb + r) * p.ld + x0 + lane;
                         if (c0ok) gp[0] = v[r][0];
@@ -407,20 +533,35 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
         }
     }
 
+    LU_T(4);
     // ---- final assembly (after everyone's write-backs and CTA 0's piv rows)
     bar_target += G;
     grid_arrive_wait(p.bar, bar_target);
     const int lane_f = tid & 31, warp_f = tid >> 5, nwarp_f = blockDim.x >> 5;
-    for (int e = warp_f; e < ne; e += nwarp_f)
+    // four entities per warp pass: their loads in flight together
+    for (int eb = warp_f * 4; eb < ne; eb += nwarp_f * 4)
     for (int x = lane_f; x < k; x += 32) {
-        const int q = pos[e];
-        double v;
-        if (q < k) {
-            const int pend = min(k, (q / b) * b + b);
-            v = x < pend ? __ldcg(p.w + (e0 + e) * p.ld + x) : __ldcg(p.piv + (int64_t)q * k + x);
-        } else {
-            v = p.w[(e0 + e) * p.ld + x];
+        double vv[4];
+        int qq[4];
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4) {
+            const int e = eb + u4;
+            const int q = e < ne ? pos[e] : -1;
+            qq[u4] = q;
+            double v = 0.0;
+            if (q >= 0 && q < k) {
+                const int pend = min(k, (q / b) * b + b);
+                v = x < pend ? __ldcg(p.w + (e0 + e) * p.ld + x) : __ldcg(p.piv + (int64_t)q * k + x);
+            } else if (q >= k) {
+                v = __ldcs(p.w + (e0 + e) * p.ld + x);
+            }
+            vv[u4] = v;
         }
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4) {
+        const int q = qq[u4];
+        const double v = vv[u4];
+        if (q < 0) continue;
         if (MODE == MODE_ROW) {
             double lv = q >= k ? v : (x < q ? v : (x == q ? 1.0 : 0.0));
             p.out_main[(int64_t)q * p.ld_main + x] = lv;
@@ -429,8 +570,11 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
             p.out_main[(int64_t)q * p.ld_main + x] = (q >= k || x <= q) ? v : 0.0;
             if (q < k) p.out_small[(int64_t)x * p.ld_small + q] = x > q ? v : (x == q ? 1.0 : 0.0);
         }
+        }
     }
     for (int e = tid; e < ne; e += blockDim.x) p.perm[pos[e]] = e0 + e;
+    LU_T(5);
+    LU_TDUMP();
 }
 
 // ---------------------------------------------------------------------------
@@ -1834,6 +1978,9 @@ static size_t lu_base_workspace(int64_t k) {
            sizeof(double) * ((size_t)2 * kLuMaxGrid * k + (size_t)k * k) + 256;
 }
 
+// L2 panel of the grid kernel: [8][ldp] doubles after the base workspace
+static inline int64_t lu_gpanel_ld(int64_t M) { return (M + 31) & ~(int64_t)31; }
+
 static size_t lu_smem_bytes(int rpc, int b, int bs) {
     return sizeof(double) * ((size_t)rpc * bs + (size_t)b * b + b + (size_t)b * kLuXC) +
            sizeof(int) * ((size_t)rpc + b) + 16;
@@ -1979,7 +2126,9 @@ static int try_run_lu_cluster(LuParams prm, void *ws, cudaStream_t stream) {
     const bool v4 = getenv("SRLU_LU_CLUSTER_V4") != nullptr;  // shared-memory rows (comparison)
     const int64_t M = prm.M;
     const int k = prm.k;
-    if (M > kLuClusterMaxM || k > 1024) return 1;
+    // the register-row kernel faults for k > 128 (measured: 220, 300, 500);
+    // wider inputs take the grid kernel (the hybrid kernel is tried first)
+    if (M > kLuClusterMaxM || k > (v4 ? 1024 : 128)) return 1;
     const size_t budget = 220 * 1024;
     LuClusterParams cp;
     cp.p = prm;
@@ -2054,11 +2203,19 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     prm.cand = (Cand *)(wsb + 256 + sizeof(double) * kLuMaxGrid);
     prm.candrow = (double *)((char *)prm.cand + sizeof(Cand) * 2 * kLuMaxGrid);
     prm.piv = prm.candrow + (size_t)2 * kLuMaxGrid * k;
+    prm.gpanel = nullptr;
+    prm.ldp = 0;
 
     int rc = try_run_lu_hybrid<MODE>(prm, ws, stream);
     if (rc <= 0) return rc;  // launched (0) or failed (<0)
-    rc = try_run_lu_cluster<MODE>(prm, ws, stream);
-    if (rc <= 0) return rc;
+    // the single-cluster kernels are kept for comparison only (opt-in): the
+    // hybrid kernel supersedes them, and the register-row one faults on some
+    // shapes (k > 128; 2048 x 60)
+    if (const char *env = getenv("SRLU_LU_CLUSTER"))  // testing knob
+        if (atoi(env)) {
+            rc = try_run_lu_cluster<MODE>(prm, ws, stream);
+            if (rc <= 0) return rc;
+        }
 
     int G = sm_count() - reserve_sms;
     if (G < 1) G = 1;
@@ -2075,10 +2232,21 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     int b = (int)k;
     while (b > 1 && lu_smem_bytes(rpc, b, b | 1) > budget) --b;
     int bs = b | 1;
+    // narrow smem panel (tall inputs): an 8-wide attribute-major L2 panel
+    const char *nogp = getenv("SRLU_LU_NO_GPANEL");  // testing knob
+    const char *fgp = getenv("SRLU_LU_GPANEL");       // testing knob: force it
+    const bool gpanel = ((b < k && b < 8) || (fgp && atoi(fgp))) && !(nogp && atoi(nogp)) &&
+                        (int64_t)rpc * ld < (1LL << 31) - 1;
+    if (gpanel) {
+        b = k < 8 ? (int)k : 8;
+        bs = 0;
+        prm.ldp = lu_gpanel_ld(M);
+        prm.gpanel = (double *)(wsb + ((lu_base_workspace(k) + 255) & ~(size_t)255));
+    }
     size_t smem = lu_smem_bytes(rpc, b, bs);
     SRLU_REQUIRE(smem <= budget, SRLU_ERR_UNSUPPORTED,
                  "lu: %lld entities per CTA do not fit in shared memory", (long long)rpc);
-    auto kern = lu_kernel<MODE>;
+    auto kern = gpanel ? lu_kernel<MODE, 8> : lu_kernel<MODE, 0>;
     SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     SRLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLuThreads, smem));
@@ -2104,10 +2272,13 @@ static size_t lu_hybrid_extra(int64_t M) {
 
 extern "C" size_t srlu_lu_workspace(int64_t M, int64_t k) {
     size_t n = lu_base_workspace(k);
+    // the grid kernel's L2 panel (same offset; the cluster paths' copy is
+    // laid out there too and never coexists with it)
+    const size_t ngp = ((n + 255) & ~(size_t)255) + sizeof(double) * 8 * (size_t)lu_gpanel_ld(M);
     if (M <= kLuClusterMaxM && k <= 1024)  // attribute-major copy for the cluster paths
         n = ((n + 255) & ~(size_t)255) + sizeof(double) * (size_t)k * lu_cluster_ldt(M) +
             lu_hybrid_extra(M);
-    return n;
+    return n > ngp ? n : ngp;
 }
 
 extern "C" int srlu_lu_rowpiv(double *y, int64_t m, int64_t k, int64_t ldy, int64_t *perm,

@@ -87,14 +87,14 @@ static bool config_try(int64_t n, int64_t l, int64_t pad, int es, int bpt, int r
     f.stage_bytes = rb * f.row_stride;
     f.xs_bytes = 2LL * rb * pad * 8;
     // leave room for the codes (~64 B per warp step, ~n/16 steps)
-    const int64_t code_est = 4 * n + 4096;
+    const int64_t code_est = env_int("SRLU_K1_GCODES", 0) ? 0 : 4 * n + 4096;
     int ns = env_int("SRLU_K1_NS", 4);
     if (ns < 2) ns = 2;
     if (ns > kMaxStages) ns = kMaxStages;
     while (ns > 2 && (size_t)(ns * f.stage_bytes + f.xs_bytes + code_est) > kSmemMax) --ns;
     f.ns = ns;
     int64_t used = ns * f.stage_bytes + f.xs_bytes;
-    if ((size_t)used + 8192 > kSmemMax) return false;
+    if ((size_t)used + (code_est ? 8192 : 256) > kSmemMax) return false;
     f.code_cap = ((int64_t)kSmemMax - used) & ~15LL;
     f.smem = used + f.code_cap;
     // workspace: header | grp[ng*32] | np[nch*ng] | wsched[nch*ng*2] | codes

@@ -145,8 +145,12 @@ def test_factor_matches_reference(P, golden):
 
 @pytest.mark.parametrize("m,k,seed,ints", [(20000, 200, 1, False), (6000, 150, 2, True),
                                            (3001, 97, 3, False), (40000, 64, 4, False)])
-def test_lu_row_pivot_panels_bit_exact(P, m, k, seed, ints):
-    """Sizes that force several panels + deferred trailing updates."""
+@pytest.mark.parametrize("gpanel", ["0", "1"])
+def test_lu_row_pivot_panels_bit_exact(P, m, k, seed, ints, gpanel, monkeypatch):
+    """Sizes that force several panels + deferred trailing updates; gpanel=1
+    forces the grid kernel's in-place (L2) panel variant used for tall inputs."""
+    monkeypatch.setenv("SRLU_LU_GPANEL", gpanel)
+    monkeypatch.setenv("SRLU_LU_NO_HYBRID", gpanel)
     from oracle import randlu as O
     g = np.random.Generator(np.random.Philox(seed))
     b = g.integers(-3, 4, size=(m, k)).astype(np.float64) if ints else g.standard_normal((m, k))
@@ -158,7 +162,10 @@ def test_lu_row_pivot_panels_bit_exact(P, m, k, seed, ints):
 
 
 @pytest.mark.parametrize("k,n,seed", [(150, 30000, 5), (97, 5003, 6), (40, 100000, 7)])
-def test_lu_col_pivot_panels_bit_exact(P, k, n, seed):
+@pytest.mark.parametrize("gpanel", ["0", "1"])
+def test_lu_col_pivot_panels_bit_exact(P, k, n, seed, gpanel, monkeypatch):
+    monkeypatch.setenv("SRLU_LU_GPANEL", gpanel)
+    monkeypatch.setenv("SRLU_LU_NO_HYBRID", gpanel)
     from oracle import randlu as O
     g = np.random.Generator(np.random.Philox(seed))
     c = g.standard_normal((k, n))
@@ -169,18 +176,21 @@ def test_lu_col_pivot_panels_bit_exact(P, k, n, seed):
     np.testing.assert_array_equal(r.U.numpy(), up)
 
 
-@pytest.mark.parametrize("m,k,seed", [(16384, 110, 8), (6000, 150, 2), (2048, 60, 9)])
+@pytest.mark.parametrize("m,k,seed", [(16384, 110, 8), (6000, 150, 2), (2048, 60, 9),
+                                      (8192, 220, 10), (4096, 128, 11), (2048, 300, 12)])
 def test_lu_cluster_and_grid_variants_agree(P, m, k, seed, monkeypatch):
-    """Shapes that fit one cluster run the DSMEM-exchange kernel; the same
-    input through the 148-CTA grid kernel (SRLU_LU_NO_CLUSTER=1) and the
-    oracle must give identical P, L, U (row) and Q, L, U (col)."""
+    """The LU kernels on one input: hybrid (default for m <= 16384), the
+    148-CTA grid kernel (SRLU_LU_NO_HYBRID=1) and its in-place-panel variant
+    (+ SRLU_LU_GPANEL=1) must give the oracle's P, L, U (row) and Q, L, U (col)."""
     from oracle import randlu as O
     g = np.random.Generator(np.random.Philox(seed))
     b = g.standard_normal((m, k))
     perm, lo, up = O.lu_row_pivot(b)
     q, lo2, up2 = O.lu_col_pivot(b.T.copy())
-    for no_cluster in ("0", "1"):
-        monkeypatch.setenv("SRLU_LU_NO_CLUSTER", no_cluster)
+    for mode in ("hybrid", "grid", "gpanel"):
+        no_cluster = mode
+        monkeypatch.setenv("SRLU_LU_NO_HYBRID", "0" if mode == "hybrid" else "1")
+        monkeypatch.setenv("SRLU_LU_GPANEL", "1" if mode == "gpanel" else "0")
         r = P.lu_row_pivot(b)
         np.testing.assert_array_equal(r.P.indices, perm, err_msg=no_cluster)
         np.testing.assert_array_equal(r.L.numpy(), lo, err_msg=no_cluster)
