@@ -139,37 +139,6 @@ __device__ __forceinline__ void fwht_block_warp_dyn512(double *blk, int pad, int
     }
 }
 
-// Value at output index q of the full pad-point transform whose bsize-point
-// blocks (nb = pad/bsize <= 16 of them, swizzled) were transformed in
-// place: the remaining stages h = bsize, 2*bsize, ... combine the blocks at
-// offset q % bsize in the reference's order.
-__device__ __forceinline__ double fwht_combine_blocks(const double *row, int bsize, int nb, int q) {
-    if (nb == 1) return row[fwht_sw(q)];
-    double u[16];
-    const int o = fwht_sw(q & (bsize - 1));
-#pragma unroll
-    for (int b = 0; b < 16; ++b) u[b] = b < nb ? row[b * bsize + o] : 0.0;
-#pragma unroll
-    for (int s = 1; s < 16; s <<= 1) {
-        if (s < nb) {
-#pragma unroll
-            for (int b = 0; b < 16; ++b) {
-                if ((b & s) == 0 && b + s < nb) {
-                    const double a = u[b], c = u[b + s];
-                    u[b] = __dadd_rn(a, c);
-                    u[b + s] = __dsub_rn(a, c);
-                }
-            }
-        }
-    }
-    const int B = q / bsize;
-    double r = u[0];
-#pragma unroll
-    for (int b = 1; b < 16; ++b)
-        if (b == B) r = u[b];
-    return r;
-}
-
 // Output-pruned cross-block stages: the value at block B, in-block offset
 // o (swizzled) of the full transform whose NB blocks (stride bsize) were
 // transformed in place.  Only the NB-1 butterfly nodes feeding that output
@@ -187,6 +156,21 @@ __device__ __forceinline__ double wht_pick(const double *row, int bsize, int o, 
         for (int i = 0; i < NB / (2 * s); ++i) u[i] = __fma_rn(sg, u[2 * i + 1], u[2 * i]);
     }
     return u[0];
+}
+
+// Value at output index q of the full pad-point transform whose bsize-point
+// blocks (nb = pad/bsize <= 16 of them, swizzled) were transformed in
+// place: the remaining stages h = bsize, 2*bsize, ... combine the blocks at
+// offset q % bsize in the reference's order (output-pruned, wht_pick).
+__device__ __forceinline__ double fwht_combine_blocks(const double *row, int bsize, int nb, int q) {
+    const int o = fwht_sw(q & (bsize - 1)), B = q / bsize;
+    switch (nb) {
+        case 1: return row[o];
+        case 2: return wht_pick<2>(row, bsize, o, B);
+        case 4: return wht_pick<4>(row, bsize, o, B);
+        case 8: return wht_pick<8>(row, bsize, o, B);
+        default: return wht_pick<16>(row, bsize, o, B);
+    }
 }
 
 }  // namespace srlu

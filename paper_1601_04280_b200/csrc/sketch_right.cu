@@ -502,7 +502,7 @@ static int dispatch_k1_dense(const T *a, int64_t m, int64_t n, int64_t lda, cons
 // CSR
 
 template <typename T, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k1_csr_kernel(
+__global__ void __launch_bounds__(WPB * 32, 3) k1_csr_kernel(
     const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
     const T *__restrict__ vals, int64_t m, const int32_t *__restrict__ row_of,
     const double *__restrict__ sign, int l, const double *__restrict__ phase,
@@ -511,6 +511,18 @@ __global__ void __launch_bounds__(WPB * 32) k1_csr_kernel(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *x = reinterpret_cast<double *>(smem_raw) + (size_t)warp * pad;
+    // +-phase folded into each entry's sign (phase[t] * sum = sum of
+    // phase[t] * terms exactly: negation commutes with rounding)
+    __shared__ unsigned phbits[8192 / 32];
+    for (int w = threadIdx.x; w < (pad + 31) / 32; w += blockDim.x) {
+        unsigned bits = 0;
+        for (int i = 0; i < 32; ++i) {
+            const int t = w * 32 + i;
+            if (t < l && phase[t] < 0.0) bits |= 1u << i;
+        }
+        phbits[w] = bits;
+    }
+    __syncthreads();
     // register FWHT (512-point blocks, swizzled) when pad >= 32
     const bool reg = pad >= 32;
     auto P = [&](int t) { return reg ? fwht_sw(t) : t; };
@@ -531,7 +543,7 @@ __global__ void __launch_bounds__(WPB * 32) k1_csr_kernel(
                 int j = indices[p];
                 double v = (double)vals[p];
                 t = row_of[j];
-                val = sign[j] < 0.0 ? -v : v;
+                val = (sign[j] < 0.0) != (((phbits[t >> 5] >> (t & 31)) & 1u) != 0) ? -v : v;
             }
             const unsigned active = __ballot_sync(0xffffffffu, valid);
             unsigned peers = 0;
@@ -547,9 +559,6 @@ __global__ void __launch_bounds__(WPB * 32) k1_csr_kernel(
             }
             __syncwarp();
         }
-        for (int t = lane; t < l; t += 32)
-            if (phase[t] < 0.0) x[P(t)] = -x[P(t)];
-        __syncwarp();
         if (reg) {
             for (int b = 0; b < nzb; ++b) fwht_block_warp_dyn512(x + b * bsize, bsize, lane);
         } else {
