@@ -197,6 +197,13 @@ constexpr int kSchedListCap = 4096;  // staged source codes per group (ints)
 
 // One pass of the simulation for group g (see sched_kernel).  src[0..cnt) =
 // this lane's bucket sources (ascending, sign in bit 31).
+// Two 16-bit step codes (column | sign << 15) as one word, laid out for a
+// cheap decode in gather_pair: bits 2-16 column of the first step, bit 0 its
+// sign, bit 1 the second step's sign, bits 17-31 its column.
+__device__ __forceinline__ uint32_t pack_pair(uint32_t lo, uint32_t hi) {
+    return ((lo & 0x7fffu) << 2) | (lo >> 15) | ((hi >> 15) << 1) | ((hi & 0x7fffu) << 17);
+}
+
 template <int PASS>
 __device__ __forceinline__ void sched_pass(const int32_t *src, int cnt, int g, int c, int nch,
                                            int es8, int bpt, int d2, int joint, int32_t *np_tab,
@@ -254,7 +261,7 @@ __device__ __forceinline__ void sched_pass(const int32_t *src, int cnt, int g, i
         uint32_t pairw = 0;
         auto emit = [&](uint32_t code) {
             if (PASS == 1) {
-                if (step & 1) out[(size_t)(step >> 1) * pstride] = pairw | (code << 16);
+                if (step & 1) out[(size_t)(step >> 1) * pstride] = pack_pair(pairw, code);
                 else pairw = code;
             }
             ++step;
@@ -368,19 +375,36 @@ __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// One element: the sign bit (bit 31 of smask) goes into the element's own
+// sign bit before the widening (exact), then acc + v — bit-identical to the
+// reference's out += s * a.
+template <typename T>
+__device__ __forceinline__ double signed_elem(const unsigned char *p, uint32_t smask) {
+    if (sizeof(T) == 4) {
+        const uint32_t f = *reinterpret_cast<const uint32_t *>(p) ^ (smask & 0x80000000u);
+        return (double)__uint_as_float(f);
+    } else {
+        const uint2 d = *reinterpret_cast<const uint2 *>(p);
+        return __hiloint2double((int)(d.y ^ (smask & 0x80000000u)), (int)d.x);
+    }
+}
+
+// Two consecutive steps of one lane from a pack_pair word (first step first).
 template <typename T, int RB>
-__device__ __forceinline__ void gather_step(const unsigned char *st, int row_stride, uint32_t c,
+__device__ __forceinline__ void gather_pair(const unsigned char *st, int row_stride, uint32_t w,
                                             double (&acc)[RB]) {
-    // acc + s*v as fma(s, v, acc), s = +-1: exact product, one rounding —
-    // bit-identical to the reference's out += s * a
-    const uint32_t col = c & 0x7fffu;
-    const double s = __hiloint2double((int)(((c & 0x8000u) << 16) | 0x3FF00000u), 0);
-    const unsigned char *p = st + col * sizeof(T);
+    const uint32_t off0 = sizeof(T) == 4 ? (w & 0x1fffcu) : ((w << 1) & 0x3fff8u);
+    const uint32_t off1 = sizeof(T) == 4 ? ((w >> 15) & 0x1fffcu) : ((w >> 14) & 0x3fff8u);
+    const uint32_t m0 = w << 31, m1 = w << 30;
+    const unsigned char *p0 = st + off0, *p1 = st + off1;
+    double v0[RB], v1[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-        const double v = (double)*reinterpret_cast<const T *>(p + r * row_stride);
-        acc[r] = __fma_rn(s, v, acc[r]);
+        v0[r] = signed_elem<T>(p0 + r * row_stride, m0);
+        v1[r] = signed_elem<T>(p1 + r * row_stride, m1);
     }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = __dadd_rn(__dadd_rn(acc[r], v0[r]), v1[r]);
 }
 
 // One gather warp's stream: per row block, per chunk, the warp's joint
@@ -415,7 +439,11 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
             for (int r = 0; r < RB; ++r) acc[b][r] = 0.0;
         for (int ch = 0; ch < d.nch; ++ch, ++it) {
             if (!(d.dbg & 8)) mbar_wait_suspend(&full[stage], ph);
-            const unsigned char *st = smem + stage * d.stage_bytes;
+            // the stage base as one opaque shared address (keeps the compiler
+            // from re-deriving smem + stage * bytes for every code)
+            uint32_t stb = smem_u32(smem + stage * d.stage_bytes);
+            asm volatile("" : "+r"(stb));
+            const unsigned char *st = (const unsigned char *)__cvta_shared_to_generic(stb);
             if (BPT == 1 || d.joint) {
                 const int2 sc = __ldg(wsched + ch * kGW + warp);
                 const int np = sc.y;
@@ -425,8 +453,7 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
 #pragma unroll
                     for (int b = 0; b < BPT; ++b) {
                         const uint32_t w = cw[base + (s2 * BPT + b) * 32];
-                        gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
-                        gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
+                        gather_pair<T, RB>(st, d.row_stride, w, acc[b]);
                     }
                 }
             } else {
@@ -438,8 +465,7 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
 #pragma unroll 4
                     for (int s2 = 0; s2 < np; ++s2) {
                         const uint32_t w = cw[base + s2 * 32];
-                        gather_step<T, RB>(st, d.row_stride, w & 0xffffu, acc[b]);
-                        gather_step<T, RB>(st, d.row_stride, w >> 16, acc[b]);
+                        gather_pair<T, RB>(st, d.row_stride, w, acc[b]);
                     }
                 }
             }
