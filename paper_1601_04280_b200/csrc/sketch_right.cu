@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
     if (tid == 0)
         for (int s = 0; s < kK1Stages && s < nchunks; ++s) issue(s, s);
 
-    int cur[BPT], end[BPT], code[BPT];
+    // code[b]: the slot's current source; nxt[b]: the one after it, loaded one
+    // step ahead so that the walk's loop condition never waits on a load
+    int cur[BPT], end[BPT], code[BPT], nxt[BPT];
     double acc[R][BPT];
 #pragma unroll
     for (int b = 0; b < BPT; ++b) {
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
         cur[b] = t < l ? bptr[t] : 0;
         end[b] = t < l ? bptr[t + 1] : 0;
         code[b] = cur[b] < end[b] ? sorted[cur[b]] : INT_MAX;
+        nxt[b] = cur[b] + 1 < end[b] ? sorted[cur[b] + 1] : INT_MAX;
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r][b] = 0.0;
     }
@@ -194,8 +197,9 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
         const int c1 = c0 + C;
 #pragma unroll
         for (int b = 0; b < BPT; ++b) {
-            int cd = code[b];
+            int cd = code[b], nx = nxt[b];
             while ((cd & 0x7FFFFFFF) < c1) {
+                const int nn = cur[b] + 2 < end[b] ? __ldg(sorted + cur[b] + 2) : INT_MAX;
                 const int cc = (cd & 0x7FFFFFFF) - c0;
                 const bool neg = cd < 0;
 #pragma unroll
@@ -204,9 +208,11 @@ __global__ void __launch_bounds__(NT) k1v2_kernel(
                     acc[r][b] = neg ? __dsub_rn(acc[r][b], v) : __dadd_rn(acc[r][b], v);
                 }
                 ++cur[b];
-                cd = cur[b] < end[b] ? __ldg(sorted + cur[b]) : INT_MAX;
+                cd = nx;
+                nx = nn;
             }
             code[b] = cd;
+            nxt[b] = nx;
         }
         __syncthreads();
         if (tid == 0 && ch + kK1Stages < nchunks) {
@@ -447,6 +453,9 @@ static int dispatch_k1v2(const T *a, int64_t m, int64_t n, int64_t lda, const in
                                           y, ldy, nonfinite, s);
     if (l <= 4096)
         return launch_k1v2<T, 1024, 4, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult,
+                                          y, ldy, nonfinite, s);
+    if (l <= 5120)  // BASELINE config 5 (l1 = 4400): 5 slots per thread, fewer registers
+        return launch_k1v2<T, 1024, 5, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult,
                                           y, ldy, nonfinite, s);
     return launch_k1v2<T, 1024, 8, 2>(a, m, n, lda, sorted, bptr, L, phase, idx, K, P, mult, y,
                                       ldy, nonfinite, s);

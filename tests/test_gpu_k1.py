@@ -78,3 +78,28 @@ def test_scheduled_k1_non_finite_flag(P, dt):
     om = P.build_composite(k, l, n, "hadamard", 1)
     with pytest.raises(ValueError):
         P.apply_sketch_right(P.Matrix.from_device(torch.from_numpy(a).cuda()), om)
+
+
+# unscheduled TMA kernel (k1v2): shapes the schedule does not take (rows over
+# 4 chunks, l1 > 3584) and every slot count it dispatches (1, 2, 4, 5, 8)
+V2_SHAPES = [
+    (40, 65536, np.float64, 4400, 550),   # config-5 shape family: 5 slots, 8 KB-pad FWHT
+    (33, 40000, np.float64, 3000, 100),   # 4 slots
+    (20, 20000, np.float64, 1500, 64),    # 2 slots, ragged chunks
+    (17, 9000, np.float64, 6000, 80),     # 8 slots
+    (50, 70000, np.float32, 900, 90),     # 1 slot, fp32 rows over 4 chunks
+]
+
+
+@pytest.mark.parametrize("m,n,dt,l,k", V2_SHAPES)
+def test_unscheduled_k1_bit_exact(P, m, n, dt, l, k, monkeypatch):
+    import torch
+    from oracle import draws as D
+    from oracle import randlu as O
+    monkeypatch.setenv("SRLU_K1_NOSCHED", "1")
+    seed = 5 + m
+    a = _wide_range(m, n, seed, dt)
+    om = P.build_composite(k, l, n, "hadamard", seed)
+    y = P.apply_sketch_right(P.Matrix.from_device(torch.from_numpy(a).cuda()), om)
+    ref = O.apply_sketch_right(a.astype(np.float64), D.build_composite(k, l, n, seed))
+    np.testing.assert_array_equal(y.numpy(), ref)
