@@ -55,6 +55,12 @@ enum { MODE_ROW = 0, MODE_COL = 1 };
 
 constexpr int kLuThreads = 512;
 constexpr int kLuRPW = 4;  // trailing update: rows per warp pass
+#ifndef SRLU_LU_PFD
+#define SRLU_LU_PFD 1  // trailing update: passes of loads in flight (2 measured: no gain)
+#endif
+#ifndef SRLU_LU_RPW
+#define SRLU_LU_RPW 4  // smem-panel kernel: rows per warp pass (8 measured slower)
+#endif
 constexpr int kLuMaxGrid = 256;
 constexpr int kLuXC = 64;  // trailing columns per chunk
 constexpr double kPivotRtol = 1e-14;  // factor.py:19
@@ -159,11 +165,27 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     // ---- thresh = PIVOT_RTOL * ||w||_F (deterministic two-level sum) ----
     {
         double ss = 0.0;
-        for (int64_t w = tid; w < (int64_t)ne * k; w += blockDim.x) {
-            int64_t e = w / k;
-            int x = (int)(w % k);
-            double v = p.w[(e0 + e) * p.ld + x];
-            ss += v * v;
+        if (p.ld == k) {  // contiguous rows: flat, four independent sums in flight
+            const double *base = p.w + e0 * p.ld;
+            const int64_t nel = (int64_t)ne * k;
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            int64_t w = tid;
+            for (; w + 3 * kLuThreads < nel; w += 4 * kLuThreads) {
+                double v4[4];
+#pragma unroll
+                for (int u4 = 0; u4 < 4; ++u4) v4[u4] = __ldcs(base + w + u4 * kLuThreads);
+#pragma unroll
+                for (int u4 = 0; u4 < 4; ++u4) s4[u4] += v4[u4] * v4[u4];
+            }
+            for (; w < nel; w += kLuThreads) s4[0] += base[w] * base[w];
+            ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        } else {
+            for (int64_t w = tid; w < (int64_t)ne * k; w += blockDim.x) {
+                int64_t e = w / k;
+                int x = (int)(w % k);
+                double v = p.w[(e0 + e) * p.ld + x];
+                ss += v * v;
+            }
         }
         // block reduce (fixed tree order)
         __shared__ double s_red[kLuThreads];
@@ -451,27 +473,29 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
             // lane): coalesced, division-free; the next pass's loads are
             // issued before this pass's arithmetic (software pipeline)
             {
-                constexpr int RPW = kLuRPW;  // 8 with the L2 panel: spills, measured slower
+                constexpr int RPW = GB ? kLuRPW : SRLU_LU_RPW;  // 8 with the L2 panel: spills
                 const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
                 const bool c0ok = lane < xc, c1ok = lane + 32 < xc;
                 const int a1i = lane + 32 < kLuXC ? lane + 32 : lane;
                 const int stride = nwarp * RPW;
-                double vn[RPW][2];
-                double pmn[RPW];  // GB: lane x holds multiplier x of row r
-                bool ln[RPW];
-                auto fetch = [&](int eb) {
+                // SRLU_LU_PFD passes of loads in flight ahead of the arithmetic
+                double vn[RPW][2], vn2[RPW][2];
+                double pmn[RPW], pmn2[RPW];  // GB: lane x holds multiplier x of row r
+                bool ln[RPW], ln2[RPW];
+                auto fetch = [&](int eb, double (&dv)[RPW][2], double (&dpm)[RPW], bool (&dl)[RPW]) {
 #pragma unroll
                     for (int r = 0; r < RPW; ++r) {
                         const int e = eb + r;
-                        ln[r] = e < ne && pos[e] >= J + bw;  // pivots are frozen
+                        dl[r] = e < ne && pos[e] >= J + bw;  // pivots are frozen
                         const double *gp = p.w + (e0 + e) * p.ld + x0 + lane;
-                        vn[r][0] = ln[r] && c0ok ? gp[0] : 0.0;
-                        vn[r][1] = ln[r] && c1ok ? gp[32] : 0.0;
-                        pmn[r] = GB && ln[r] && lane < bw ? panel[(int64_t)e * es + lane * xs] : 0.0;
+                        dv[r][0] = dl[r] && c0ok ? gp[0] : 0.0;
+                        dv[r][1] = dl[r] && c1ok ? gp[32] : 0.0;
+                        dpm[r] = GB && dl[r] && lane < bw ? panel[(int64_t)e * es + lane * xs] : 0.0;
                     }
                 };
                 int eb = warp * RPW;
-                if (eb < ne) fetch(eb);
+                if (eb < ne) fetch(eb, vn, pmn, ln);
+                if (SRLU_LU_PFD > 1 && eb + stride < ne) fetch(eb + stride, vn2, pmn2, ln2);
                 for (; eb < ne; eb += stride) {
                     double v[RPW][2];
                     double pm[RPW];
@@ -483,7 +507,18 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                         live[r] = ln[r];
                         pm[r] = pmn[r];
                     }
-                    if (eb + stride < ne) fetch(eb + stride);
+                    if (SRLU_LU_PFD > 1) {
+#pragma unroll
+                        for (int r = 0; r < RPW; ++r) {
+                            vn[r][0] = vn2[r][0];
+                            vn[r][1] = vn2[r][1];
+                            ln[r] = ln2[r];
+                            pmn[r] = pmn2[r];
+                        }
+                        if (eb + 2 * stride < ne) fetch(eb + 2 * stride, vn2, pmn2, ln2);
+                    } else if (eb + stride < ne) {
+                        fetch(eb + stride, vn, pmn, ln);
+                    }
                     if (GB) {  // all lanes shuffle (stores below are gated by live)
 #pragma unroll
                         for (int ls = 0; ls < (GB > 0 ? GB : 1); ++ls) {
@@ -503,20 +538,21 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                             }
                         }
                     }
-#pragma unroll
-                    for (int r = 0; r < RPW; ++r) {
-                        if (!live[r] || GB) continue;
-                        const double *pe = panel + (eb + r) * bs;
+                    if (!GB) {  // steps outer, rows inner: one Ach load per step
+                        const double *pe = panel + eb * bs;
                         for (int ls = 0; ls < bw; ++ls) {
-                            const double pv = pe[ls];
                             const double a0 = Ach[ls * kLuXC + lane];
                             const double a1 = Ach[ls * kLuXC + a1i];
-                            if (MODE == MODE_ROW) {
-                                v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
-                                v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
-                            } else {
-                                v[r][0] = __dsub_rn(v[r][0], __dmul_rn(a0, pv));
-                                v[r][1] = __dsub_rn(v[r][1], __dmul_rn(a1, pv));
+#pragma unroll
+                            for (int r = 0; r < RPW; ++r) {
+                                const double pv = pe[r * bs + ls];  // dead rows: unused
+                                if (MODE == MODE_ROW) {
+                                    v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
+                                    v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
+                                } else {
+                                    v[r][0] = __dsub_rn(v[r][0], __dmul_rn(a0, pv));
+                                    v[r][1] = __dsub_rn(v[r][1], __dmul_rn(a1, pv));
+                                }
                             }
                         }
                     }

@@ -1,4 +1,5 @@
-// Phase timing of the cluster LU (rank 0, thread 0 clock64 sums).
+// Phase timing of the LU kernels (rank 0, thread 0 clock64 sums).
+// Usage: tools/lu_trace m k [col]
 // Build: nvcc -DSRLU_LU_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false \
 //   -std=c++17 tools/lu_trace.cu paper_1601_04280_b200/csrc/abi.cu -o tools/lu_trace
 #include <cstdio>
@@ -30,7 +31,9 @@ int main(int argc, char **argv) {
         cudaMemcpy(y, y0, h.size() * 8, cudaMemcpyDeviceToDevice);
         cudaMemcpyToSymbol(g_lu_trace, zero, sizeof(zero));
         cudaEventRecord(e0);
-        int rc = srlu_lu_rowpiv(y, m, k, k, perm, L, k, U, k, 0, ws, wsb, 0);
+        const bool col = argc > 3 && argv[3][0] == 'c';  // col mode: m entities = columns
+        int rc = col ? srlu_lu_colpiv(y, m, k, k, perm, U, k, L, k, 0, ws, wsb, 0)
+                     : srlu_lu_rowpiv(y, m, k, k, perm, L, k, U, k, 0, ws, wsb, 0);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
