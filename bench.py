@@ -388,6 +388,8 @@ def main():
     line = {
         "metric": metric, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
+        "step_ms": {"min": round(float(np.min(times)), 4), "median": round(float(np.median(times)), 4),
+                    "max": round(float(np.max(times)), 4)},
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, generated on device; BASELINE config shapes)",
         "config": {"workload": workload, "config_id": args.config, "m": shape[0], "n": shape[1],
