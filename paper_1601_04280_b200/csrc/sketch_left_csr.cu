@@ -24,40 +24,96 @@ __global__ void csr_col_count_kernel(const int32_t *__restrict__ indices, int64_
         atomicAdd(cnt + indices[p], 1);
 }
 
-// single CTA exclusive scan (int counts -> int64 pointers)
-__global__ void csr_col_scan_kernel(const int *__restrict__ cnt, int64_t n,
-                                    int64_t *__restrict__ colptr, int *__restrict__ maxcnt) {
-    __shared__ int64_t part[1024];
-    __shared__ int pmax[1024];
-    const int nt = blockDim.x;
+// single CTA exclusive scan (int counts -> int64 pointers): per-thread
+// chunk sums, a two-level warp-shuffle scan of the 1024 partials, then each
+// thread writes its chunk (4-wide independent loads)
+__global__ void __launch_bounds__(1024) csr_col_scan_kernel(const int *__restrict__ cnt, int64_t n,
+                                                            int64_t *__restrict__ colptr,
+                                                            int *__restrict__ maxcnt) {
+    __shared__ int64_t wsum[32];
+    __shared__ int wmax[32];
+    const int nt = blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t per = (n + nt - 1) / nt;
     const int64_t lo = threadIdx.x * per, hi = min(n, lo + per);
-    int64_t s = 0;
+    int64_t sum = 0;
     int mx = 0;
     for (int64_t j = lo; j < hi; ++j) {
-        s += cnt[j];
-        mx = max(mx, cnt[j]);
+        const int c = __ldg(cnt + j);
+        sum += c;
+        mx = max(mx, c);
     }
-    part[threadIdx.x] = s;
-    pmax[threadIdx.x] = mx;
+    int64_t incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 31) wsum[warp] = incl;
+    if (lane == 0) wmax[warp] = mx;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t run = 0;
-        int m2 = 0;
-        for (int i = 0; i < nt; ++i) {
-            int64_t c = part[i];
-            part[i] = run;
-            run += c;
-            m2 = max(m2, pmax[i]);
+    if (warp == 0) {
+        const int nw = nt >> 5;
+        int64_t v = lane < nw ? wsum[lane] : 0;
+        int m2 = lane < nw ? wmax[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, v, d);
+            if (lane >= d) v += y;
         }
-        colptr[n] = run;
-        *maxcnt = m2;
+        m2 = __reduce_max_sync(0xffffffffu, m2);
+        wsum[lane] = v;  // inclusive warp totals
+        if (lane == 31) {
+            colptr[n] = v;
+            *maxcnt = m2;
+        }
     }
     __syncthreads();
-    int64_t run = part[threadIdx.x];
+    int64_t run = (warp > 0 ? wsum[warp - 1] : 0) + incl - sum;
     for (int64_t j = lo; j < hi; ++j) {
         colptr[j] = run;
-        run += cnt[j];
+        run += __ldg(cnt + j);
+    }
+}
+
+// Entry codec.  16 bytes: {(t << 32) | q, double bits of +-v}.  8 bytes
+// (fp32 values whose key (t, q) fits 32 bits — BASELINE config 4): one u64
+// ((t << qb | q) << 32 | float bits of +-v); +-v is exact in fp32 and is
+// widened at the fold, like the reference's upcast.  The mode is decided on
+// the device from the largest position q (mode[0] = qb + 1, or 0 = 16 bytes).
+__global__ void csr_mode_kernel(const int32_t *__restrict__ inv_perm, int64_t rows, int l,
+                                int is_f32, int *mode) {
+    int mx = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, inv_perm[r]);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) atomicMax(mode + 1, mx);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(mode + 2, 1) == (int)gridDim.x - 1) {
+        __threadfence();
+        const int qmax = atomicAdd(mode + 1, 0);
+        const int qb = qmax > 0 ? 32 - __clz(qmax) : 1;
+        const int tb = l > 1 ? 32 - __clz(l - 1) : 1;
+        mode[0] = (is_f32 && qb + tb <= 32) ? qb + 1 : 0;
+    }
+}
+
+__device__ __forceinline__ void ent_read(const void *ent, int64_t i, int mode, unsigned &t,
+                                         int &q, double &v) {
+    if (mode) {
+        const unsigned long long w = reinterpret_cast<const unsigned long long *>(ent)[i];
+        const unsigned key = (unsigned)(w >> 32);
+        const int qb = mode - 1;
+        t = key >> qb;
+        q = (int)(key & ((1u << qb) - 1u));
+        v = (double)__uint_as_float((unsigned)w);
+    } else {
+        const ulonglong2 e = reinterpret_cast<const ulonglong2 *>(ent)[i];
+        t = (unsigned)(e.x >> 32);
+        q = (int)(unsigned)e.x;
+        v = __longlong_as_double((long long)e.y);
     }
 }
 
@@ -68,8 +124,9 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
                                 const int32_t *__restrict__ row_of2,
                                 const double *__restrict__ sign2,
                                 const int64_t *__restrict__ colptr, int *__restrict__ fill,
-                                ulonglong2 *__restrict__ ent) {
+                                void *__restrict__ ent, const int *__restrict__ modep) {
     const int lane = threadIdx.x & 31;
+    const int mode = sizeof(T) == 4 ? *modep : 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = warp; r < rows; r += nwarp) {
@@ -77,11 +134,19 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
         const unsigned long long key =
             ((unsigned long long)(unsigned)row_of2[q] << 32) | (unsigned)q;
         const bool neg = sign2[q] < 0.0;
+        const unsigned key8 = mode ? ((unsigned)row_of2[q] << (mode - 1)) | (unsigned)q : 0u;
         for (int64_t p = indptr[r] + lane; p < indptr[r + 1]; p += 32) {
             const int j = indices[p];
             const int64_t slot = colptr[j] + atomicAdd(fill + j, 1);
-            const double v = (double)vals[p];
-            ent[slot] = make_ulonglong2(key, (unsigned long long)__double_as_longlong(neg ? -v : v));
+            if (mode) {
+                const float f = (float)vals[p];
+                reinterpret_cast<unsigned long long *>(ent)[slot] =
+                    ((unsigned long long)key8 << 32) | __float_as_uint(neg ? -f : f);
+            } else {
+                const double v = (double)vals[p];
+                reinterpret_cast<ulonglong2 *>(ent)[slot] =
+                    make_ulonglong2(key, (unsigned long long)__double_as_longlong(neg ? -v : v));
+            }
         }
     }
 }
@@ -89,9 +154,12 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
 // One CTA per column (grid-stride); handles columns with lo < count <= CAP.
 template <int CAP>
 __global__ void __launch_bounds__(256) csr_col_project_kernel(
-    const int64_t *__restrict__ colptr, const ulonglong2 *__restrict__ ent, int64_t n, int l,
-    int pad, const double *__restrict__ phase, const int32_t *__restrict__ idx, int k,
-    double mult, double *__restrict__ out, int64_t ldo, int *flags, int lo) {
+    const int64_t *__restrict__ colptr, const void *__restrict__ ent, const int *__restrict__ modep,
+    int64_t n, int l, int pad, const double *__restrict__ phase, const int32_t *__restrict__ idx,
+    int k, double mult, double *__restrict__ out, int64_t ldo, int *flags, int lo,
+    const int *__restrict__ maxcnt) {
+    const int mode = *modep;
+    if (maxcnt != nullptr && *maxcnt <= lo) return;  // no column for this launch
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *x = reinterpret_cast<double *>(smem_raw);                          // pad
     unsigned long long *sk = reinterpret_cast<unsigned long long *>(x + pad);  // CAP
@@ -114,9 +182,12 @@ __global__ void __launch_bounds__(256) csr_col_project_kernel(
         while (n2 < cnt) n2 <<= 1;
         for (int i = threadIdx.x; i < n2; i += blockDim.x) {
             if (i < cnt) {
-                const ulonglong2 e = ent[p0 + i];
-                sk[i] = e.x;
-                sv[i] = __longlong_as_double((long long)e.y);
+                unsigned t;
+                int q;
+                double v;
+                ent_read(ent, p0 + i, mode, t, q, v);
+                sk[i] = ((unsigned long long)t << 32) | (unsigned)q;
+                sv[i] = v;
             } else {
                 sk[i] = ~0ULL;
                 sv[i] = 0.0;
@@ -173,11 +244,12 @@ __global__ void __launch_bounds__(256) csr_col_project_kernel(
 // put in ascending q by the thread that folds that bucket (insertion sort),
 // so every bucket sum is the reference's sequential sum in PA-row order.
 template <int CAP, int NT>
-__global__ void __launch_bounds__(NT) csr_col_bucket_kernel(
-    const int64_t *__restrict__ colptr, const ulonglong2 *__restrict__ ent, int64_t n, int l,
-    int pad, const double *__restrict__ phase, const int32_t *__restrict__ idx, int k,
-    double mult, double *__restrict__ out, int64_t ldo) {
+__global__ void __launch_bounds__(NT, 1024 / NT) csr_col_bucket_kernel(
+    const int64_t *__restrict__ colptr, const void *__restrict__ ent, const int *__restrict__ modep,
+    int64_t n, int l, int pad, const double *__restrict__ phase, const int32_t *__restrict__ idx,
+    int k, double mult, double *__restrict__ out, int64_t ldo) {
     constexpr int PER = CAP / NT;
+    const int mode = *modep;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *x = reinterpret_cast<double *>(smem_raw);   // pad
     double *sv = x + pad;                               // CAP
@@ -196,22 +268,22 @@ __global__ void __launch_bounds__(NT) csr_col_bucket_kernel(
         if (cnt > CAP) continue;  // uniform: the bitonic launch takes it
         for (int t = threadIdx.x; t <= l; t += NT) base[t] = 0;
         __syncthreads();
-        unsigned long long ek[PER];
+        unsigned et[PER];
+        int eq[PER];
         double evv[PER];
         int off[PER];
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
             const int e = threadIdx.x + r * NT;
             off[r] = -1;
-            ek[r] = 0;
+            et[r] = 0;
+            eq[r] = 0;
             evv[r] = 0.0;
-            if (e < cnt) {
-                const ulonglong2 v = ent[p0 + e];
-                ek[r] = v.x;
-                evv[r] = __longlong_as_double((long long)v.y);
-                off[r] = atomicAdd(base + (int)(v.x >> 32), 1);
-            }
+            if (e < cnt) ent_read(ent, p0 + e, mode, et[r], eq[r], evv[r]);
         }
+#pragma unroll
+        for (int r = 0; r < PER; ++r)
+            if (threadIdx.x + r * NT < cnt) off[r] = atomicAdd(base + (int)et[r], 1);
         __syncthreads();
         // exclusive scan of the l bucket counts (chunk per thread)
         const int c0 = threadIdx.x * chunk;
@@ -240,8 +312,8 @@ __global__ void __launch_bounds__(NT) csr_col_bucket_kernel(
 #pragma unroll
         for (int r = 0; r < PER; ++r)
             if (off[r] >= 0) {
-                const int pos = base[(int)(ek[r] >> 32)] + off[r];
-                sq[pos] = (int)(unsigned)ek[r];
+                const int pos = base[(int)et[r]] + off[r];
+                sq[pos] = eq[r];
                 sv[pos] = evv[r];
             }
         __syncthreads();
@@ -282,9 +354,9 @@ __global__ void __launch_bounds__(NT) csr_col_bucket_kernel(
 }
 
 struct CsrWs {
-    int *cnt, *fill, *maxcnt;
+    int *cnt, *fill, *maxcnt, *mode;
     int64_t *colptr;
-    ulonglong2 *ent;
+    void *ent;
 };
 
 static size_t csr_ws_layout(int64_t n, int64_t nnz, char *base, CsrWs *w) {
@@ -298,8 +370,9 @@ static size_t csr_ws_layout(int64_t n, int64_t nnz, char *base, CsrWs *w) {
     p = take(sizeof(int) * n);             if (w) w->cnt = (int *)p;
     p = take(sizeof(int) * n);             if (w) w->fill = (int *)p;
     p = take(sizeof(int) * 4);             if (w) w->maxcnt = (int *)p;
+    p = take(sizeof(int) * 4);             if (w) w->mode = (int *)p;
     p = take(sizeof(int64_t) * (n + 1));   if (w) w->colptr = (int64_t *)p;
-    p = take(sizeof(ulonglong2) * (nnz > 0 ? nnz : 1)); if (w) w->ent = (ulonglong2 *)p;
+    p = take(sizeof(ulonglong2) * (nnz > 0 ? nnz : 1)); if (w) w->ent = (void *)p;
     return off;
 }
 
@@ -313,6 +386,15 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
     csr_ws_layout(n, nnz, (char *)ws, &w);
     SRLU_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int) * n, s));
     SRLU_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int) * n, s));
+    SRLU_CUDA(cudaMemsetAsync(w.mode, 0, sizeof(int) * 4, s));
+    if (rows > 0) {
+        int64_t blocks = ceil_div(rows, 256);
+        if (blocks > 148 * 4) blocks = 148 * 4;
+        csr_mode_kernel<<<(unsigned)blocks, 256, 0, s>>>(inv_perm, rows, (int)l2,
+                                                         sizeof(T) == 4 && !getenv("SRLU_CSR_E16"),
+                                                         w.mode);
+        SRLU_CHECK_LAUNCH("csr_mode_kernel");
+    }
     if (nnz > 0) {
         csr_col_count_kernel<<<148 * 8, 256, 0, s>>>(indices, nnz, w.cnt);
         SRLU_CHECK_LAUNCH("csr_col_count_kernel");
@@ -324,21 +406,31 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         if (blocks > 148 * 16) blocks = 148 * 16;
         csr_fill_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(indptr, indices, vals, rows, inv_perm,
                                                            row_of2, sign2, w.colptr, w.fill,
-                                                           w.ent);
+                                                           w.ent, w.mode);
         SRLU_CHECK_LAUNCH("csr_fill_kernel");
     }
     // columns with <= 2048 entries: bucket counting sort (high occupancy);
     // longer ones (<= 8192) in a bitonic launch; longer still -> flags |= 2
     const int64_t grid = n < 148 * 16 ? n : 148 * 16;
     {
-        constexpr int CAP = 2048, NT = 256;
+        constexpr int CAP = 2048;
         size_t smem = sizeof(double) * pad2 + (sizeof(double) + sizeof(int)) * CAP +
                       sizeof(int) * (l2 + 1);
         SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left_csr: pad2 too large");
-        SRLU_CUDA(cudaFuncSetAttribute(csr_col_bucket_kernel<CAP, NT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        csr_col_bucket_kernel<CAP, NT><<<(unsigned)grid, NT, smem, s>>>(
-            w.colptr, w.ent, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo);
+        const char *ntenv = getenv("SRLU_CSR_NT");  // testing knob: 512
+        if (ntenv && atoi(ntenv) == 512) {
+            SRLU_CUDA(cudaFuncSetAttribute(csr_col_bucket_kernel<CAP, 512>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            csr_col_bucket_kernel<CAP, 512><<<(unsigned)grid, 512, smem, s>>>(
+                w.colptr, w.ent, w.mode, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out,
+                ldo);
+        } else {
+            SRLU_CUDA(cudaFuncSetAttribute(csr_col_bucket_kernel<CAP, 256>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            csr_col_bucket_kernel<CAP, 256><<<(unsigned)grid, 256, smem, s>>>(
+                w.colptr, w.ent, w.mode, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out,
+                ldo);
+        }
         SRLU_CHECK_LAUNCH("csr_col_bucket_kernel");
     }
     {
@@ -347,8 +439,8 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel<kCsrColCap>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         csr_col_project_kernel<kCsrColCap><<<(unsigned)(grid < 148 ? grid : 148), 256, smem, s>>>(
-            w.colptr, w.ent, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
-            flags, 2048);
+            w.colptr, w.ent, w.mode, n, (int)l2, (int)pad2, phase2, idx2, (int)k2, mult2, out, ldo,
+            flags, 2048, w.maxcnt);
     }
     SRLU_CHECK_LAUNCH("csr_col_project_kernel");
     return SRLU_OK;

@@ -82,7 +82,7 @@ static bool config_try(int64_t n, int64_t l, int64_t pad, int es, int bpt, int r
     // each slot on its own step sequence.  One slot: consecutive buckets, so
     // the FWHT stages h < 32 run on the accumulators directly.
     f.sorted = env_int("SRLU_K1_SORT", bpt >= 2 ? 1 : 0) != 0;
-    f.joint = !f.sorted;
+    f.joint = env_int("SRLU_K1_JOINT", f.sorted ? 0 : 1) != 0;  // testing knob
     f.row_stride = (c + f.zpad) * es;
     f.stage_bytes = rb * f.row_stride;
     f.xs_bytes = 2LL * rb * pad * 8;

@@ -330,8 +330,10 @@ def test_config2_full_size_vs_oracle(P):
                ref["core"], ref["red_l"], ref["red_a"], ref["L1"])
 
 
-def test_csr_long_columns_bit_exact(P):
-    """Columns longer than the 2048-entry fast path (second launch) stay exact."""
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_csr_long_columns_bit_exact(P, dt):
+    """Columns longer than the 2048-entry fast path (second launch) stay exact
+    (fp32 values: the compact 8-byte entries)."""
     from scipy.sparse import csr_array
     from oracle import randlu as O
     g = np.random.Generator(np.random.Philox(31))
@@ -340,6 +342,7 @@ def test_csr_long_columns_bit_exact(P):
     d[g.random((m, n)) < 0.97] = 0.0
     d[g.random(m) < 0.6, 7] = g.standard_normal(1)[0]      # ~3600 entries in column 7
     d[:, 11] = g.standard_normal(m)                          # dense column 11
+    d = d.astype(dt)
     prm = dict(r=6, k1=14, l1=56, k2=22, l2=88, seed=5)
     res = P.sparse_randomized_lu(P.Matrix.sparse(csr_array(d)), P.RandLuParams(**prm), keep=True)
     ref = O.sparse_randomized_lu(csr_array(d), prm, keep=True)
@@ -348,7 +351,8 @@ def test_csr_long_columns_bit_exact(P):
     np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
 
 
-def test_csr_crowded_buckets_bit_exact(P):
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_csr_crowded_buckets_bit_exact(P, dt):
     """Few stage-2 buckets, ~1600 entries per column: long same-bucket runs whose
     fold order (ascending PA row) matters; values span many binades."""
     from scipy.sparse import csr_array
@@ -357,6 +361,7 @@ def test_csr_crowded_buckets_bit_exact(P):
     m, n = 20000, 64
     d = g.standard_normal((m, n)) * np.exp2(g.integers(-30, 30, size=(m, n)))
     d[g.random((m, n)) < 0.92] = 0.0
+    d = d.astype(dt)
     prm = dict(r=4, k1=8, l1=40, k2=12, l2=24, seed=3)
     res = P.sparse_randomized_lu(P.Matrix.sparse(csr_array(d)), P.RandLuParams(**prm), keep=True)
     ref = O.sparse_randomized_lu(csr_array(d), prm, keep=True)
