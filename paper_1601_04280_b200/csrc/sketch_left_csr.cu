@@ -129,23 +129,57 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
     const int mode = sizeof(T) == 4 ? *modep : 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < rows; r += nwarp) {
-        const int q = inv_perm[r];
-        const unsigned long long key =
-            ((unsigned long long)(unsigned)row_of2[q] << 32) | (unsigned)q;
-        const bool neg = sign2[q] < 0.0;
-        const unsigned key8 = mode ? ((unsigned)row_of2[q] << (mode - 1)) | (unsigned)q : 0u;
-        for (int64_t p = indptr[r] + lane; p < indptr[r + 1]; p += 32) {
-            const int j = indices[p];
-            const int64_t slot = colptr[j] + atomicAdd(fill + j, 1);
-            if (mode) {
-                const float f = (float)vals[p];
-                reinterpret_cast<unsigned long long *>(ent)[slot] =
-                    ((unsigned long long)key8 << 32) | __float_as_uint(neg ? -f : f);
-            } else {
-                const double v = (double)vals[p];
-                reinterpret_cast<ulonglong2 *>(ent)[slot] =
-                    make_ulonglong2(key, (unsigned long long)__double_as_longlong(neg ? -v : v));
+    constexpr int U = 4;  // 32-entry chunks of one row in flight together
+    // 32 rows per warp pass: lane i fetches row rb+i's metadata, then the
+    // warp walks the rows in turn, U chunks of each row's loads in flight
+    for (int64_t rb = warp * 32; rb < rows; rb += nwarp * 32) {
+        const int64_t rr = rb + lane;
+        int64_t mp0 = 0, mp1 = 0;
+        unsigned long long mkey = 0;
+        unsigned mkey8 = 0;
+        bool mneg = false;
+        if (rr < rows) {
+            const int q = inv_perm[rr];
+            const int t = row_of2[q];
+            mkey = ((unsigned long long)(unsigned)t << 32) | (unsigned)q;
+            mkey8 = mode ? ((unsigned)t << (mode - 1)) | (unsigned)q : 0u;
+            mneg = sign2[q] < 0.0;
+            mp0 = indptr[rr];
+            mp1 = indptr[rr + 1];
+        }
+        const int nr = (int)min((int64_t)32, rows - rb);
+        for (int i = 0; i < nr; ++i) {
+            const int64_t p0 = __shfl_sync(0xffffffffu, mp0, i);
+            const int64_t p1 = __shfl_sync(0xffffffffu, mp1, i);
+            const unsigned long long key = __shfl_sync(0xffffffffu, mkey, i);
+            const unsigned key8 = __shfl_sync(0xffffffffu, mkey8, i);
+            const bool neg = __shfl_sync(0xffffffffu, (int)mneg, i) != 0;
+            for (int64_t pb = p0; pb < p1; pb += 32 * U) {
+                int j[U];
+                T v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t p = pb + u * 32 + lane;
+                    j[u] = p < p1 ? indices[p] : -1;
+                    v[u] = p < p1 ? vals[p] : T(0);
+                }
+                int64_t slot[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    slot[u] = j[u] >= 0 ? colptr[j[u]] + atomicAdd(fill + j[u], 1) : 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (j[u] < 0) continue;
+                    if (mode) {
+                        const float f = (float)v[u];
+                        reinterpret_cast<unsigned long long *>(ent)[slot[u]] =
+                            ((unsigned long long)key8 << 32) | __float_as_uint(neg ? -f : f);
+                    } else {
+                        const double d = (double)v[u];
+                        reinterpret_cast<ulonglong2 *>(ent)[slot[u]] = make_ulonglong2(
+                            key, (unsigned long long)__double_as_longlong(neg ? -d : d));
+                    }
+                }
             }
         }
     }
