@@ -19,6 +19,7 @@ synchronises once per attempt (rank test + non-finite flag).
 from __future__ import annotations
 
 import logging
+import os
 import math
 import threading
 from dataclasses import dataclass, field as dc_field
@@ -216,7 +217,12 @@ def _stage_events(dev, n):
 def _side_stream(dev):
     key = torch.device(dev).index
     if key not in _SIDE_STREAMS:
-        _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev)
+        # high priority (testing knob SRLU_SIDE_PRIO=0 turns it off): the
+        # side stream's small latency-bound kernels (Omega2 draws, QR/pinv,
+        # rank test) take the next free SM slot ahead of the main stream's
+        # queued CTAs instead of waiting for a whole streaming grid to drain
+        prio = -1 if os.environ.get("SRLU_SIDE_PRIO", "1") != "0" else 0
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev, priority=prio)
     return _SIDE_STREAMS[key]
 
 
