@@ -161,12 +161,73 @@ def sparse_randomized_lu(a, params: RandLuParams, *, keep: bool = False) -> Rand
     return _pipeline(a, params, keep)
 
 
-def gaussian_randomized_lu(a, params):  # randlu.py:216-219
-    raise NotImplementedError("the dense-Gaussian baseline is out of scope of the B200 path "
-                              "(SURVEY.md §2.1 row 9)")
+def gaussian_randomized_lu(a, params: RandLuParams, keep: bool = False) -> RandLuResult:
+    """randlu.py:216-219: the same pipeline with dense Gaussian projections
+    G1 (k1 x n) and G2 (k2 x m) applied by plain FP64 matrix products
+    (randlu.py:184-205) — the paper's comparison baseline.  The draws are
+    numpy's Philox(seed) standard normals (host, then uploaded); the products
+    run on cuBLAS DGEMM (cuSPARSE SpMM for CSR); the LUs, pseudo-inverse and
+    rank test are the same kernels as the sparse path."""
+    a = a if isinstance(a, Matrix) else Matrix(a)
+    return _pipeline(a, params, keep, gaussian=True)
 
 
-def _pipeline(a: Matrix, params: RandLuParams, keep: bool) -> RandLuResult:
+def _gaussian_host(k, n, seed):
+    """randlu.py:197-205 (real field)."""
+    g = np.random.Generator(np.random.Philox(seed))
+    return g.standard_normal((k, n))
+
+
+def _attempt_gaussian(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandLuResult:
+    m, n = a.shape
+    dev = a.device
+    k1, k2 = params.k1, params.k2
+    main = torch.cuda.current_stream(dev)
+    ev = _stage_events(dev, len(STAGES) + 1)
+    ev[0].record(main)
+    g1 = torch.from_numpy(_gaussian_host(k1, n, params.seed + 2 * attempt)).to(dev)
+    g2 = torch.from_numpy(_gaussian_host(k2, m, params.seed + 2 * attempt + 1)).to(dev)
+    if a.is_sparse:
+        indptr, indices, values = a.raw
+        rows = torch.repeat_interleave(torch.arange(m, device=dev), indptr.diff())
+        a_op = torch.sparse_coo_tensor(torch.stack([rows, indices.long()]), values.double(),
+                                       (m, n), check_invariants=False).coalesce()
+    else:
+        a_op = a.raw.double() if a.raw.dtype != torch.float64 else a.raw
+    if not bool(torch.isfinite(a_op.values() if a.is_sparse else a_op).all()):
+        raise ValueError("matrix entries must be finite")
+    y = (a_op @ g1.t()).contiguous()                      # A . G1^T, m x k1
+    ev[1].record(main)
+    y_keep = y.clone() if keep else None
+    perm, l1, _ = lu_row_pivot_dev(y)
+    ev[2].record(main)
+    red_lT = (l1.t() @ g2.t()).contiguous()               # (G2 . L1)^T, k1 x k2
+    g2p = torch.empty_like(g2)
+    g2p[:, perm] = g2                                      # G2 . (P A) = G2p . A
+    red_aT = (a_op.t() @ g2p.t()).contiguous() if a.is_sparse else \
+        (a_op.t() @ g2p.t()).contiguous()                  # (G2 P A)^T, n x k2
+    ev[3].record(main)
+    pinv_t, stats = pinv_dev(red_lT)
+    core_t = dgemm(red_aT, pinv_t)
+    ev[4].record(main)
+    core_keep = core_t.clone() if keep else None
+    q, lt, ut = lu_col_pivot_dev(core_t)
+    l_final = dgemm(l1, lt)
+    ev[5].record(main)
+    ev[5].synchronize()
+    check_rank(stats.cpu().numpy())
+    elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
+    res = RandLuResult(P=Permutation(perm.cpu().numpy(), perm, validate=False),
+                       Q=Permutation(q.cpu().numpy(), q, validate=False),
+                       L=Matrix.from_device(l_final), U=_wrap(ut.t()), elapsed=elapsed,
+                       attempt=attempt)
+    if keep:
+        res.extras = dict(Y=y_keep, L1=l1, red_l=red_lT.t(), red_a=red_aT.t(), pinv=pinv_t.t(),
+                          core=core_keep.t(), Lt=lt, g1=g1, g2=g2)
+    return res
+
+
+def _pipeline(a: Matrix, params: RandLuParams, keep: bool, gaussian: bool = False) -> RandLuResult:
     m, n = a.shape
     params.check_against(m, n)
     if a.field != params.field:
@@ -178,7 +239,7 @@ def _pipeline(a: Matrix, params: RandLuParams, keep: bool) -> RandLuResult:
     last = None
     for attempt in range(1 + MAX_RESAMPLES):
         try:
-            res = _attempt(a, params, attempt, keep)
+            res = (_attempt_gaussian if gaussian else _attempt)(a, params, attempt, keep)
             t1 = torch.cuda.Event(enable_timing=True)
             t1.record()
             t1.synchronize()
