@@ -86,6 +86,21 @@ int srlu_build_composite_k1(uint64_t seed, int64_t k, int64_t l, int64_t n, int3
                             void *ws, size_t ws_bytes, int dtype, void *sched, size_t sched_bytes,
                             srlu_stream_t stream);
 
+/* build_composite_k1 followed, on the same stream and in the same call, by
+ * *nonfinite = 0 and the stage-1 sketch Y = A . Omega^* of a dense A
+ * (srlu_sketch_right_dense_sched when sched != NULL, else
+ * srlu_sketch_right_dense): randlu.py:252-253 (build_composite, then
+ * apply_sketch_right) as one host entry.  mult = scale / sqrt(pad) with
+ * scale = sqrt(pad / k) (sketch.py:330). */
+int srlu_composite_sketch_right_dense(uint64_t seed, int64_t k, int64_t l, int64_t n,
+                                      int32_t *row_of, double *sign, int32_t *sorted,
+                                      int32_t *bucket_ptr, double *phase, int32_t *sample_idx,
+                                      int64_t *pad, void *staging, size_t staging_bytes, void *ws,
+                                      size_t ws_bytes, void *sched, size_t sched_bytes,
+                                      const void *a, int dtype, int64_t m, int64_t lda,
+                                      double mult, double *y, int64_t ldy, int *nonfinite,
+                                      srlu_stream_t stream);
+
 /* build_sem(l, n, seed) on the DEVICE: row_of[n] in [0,l), sign[n] = +-1.
  * Bit-exact with numpy Generator(Philox(seed)).integers (Lemire). */
 size_t srlu_draw_sem_workspace(int64_t n, int64_t l);

@@ -43,6 +43,9 @@ SIGNATURES = {
     "srlu_build_composite": (INT, [U64, I64, I64, I64, P, P, P, P, P, P, P, P, SZ, P, SZ, P]),
     "srlu_build_composite_k1": (INT, [U64, I64, I64, I64, P, P, P, P, P, P, P, P, SZ, P, SZ,
                                       INT, P, SZ, P]),
+    "srlu_composite_sketch_right_dense": (INT, [U64, I64, I64, I64, P, P, P, P, P, P, P, P, SZ,
+                                                P, SZ, P, SZ, P, INT, I64, I64, DBL, P, I64, P,
+                                                P]),
     "srlu_draw_sem": (INT, [U64, I64, I64, P, P, P, SZ, P]),
     "srlu_sem_plan_workspace": (SZ, [I64, I64]),
     "srlu_sem_plan": (INT, [P, P, I64, I64, P, P, P, SZ, P]),
@@ -113,7 +116,7 @@ def lib():
 class _LaunchCounter:
     """Number of libsrlu kernels enqueued (bench.py's ``gpu_launches``)."""
 
-    PER_CALL = {"build_sem": 3, "sem_plan": 4, "build_composite": 7, "build_composite_k1": 9, "sketch_right_dense": 1, "sketch_right_csr": 1,
+    PER_CALL = {"build_sem": 3, "sem_plan": 4, "build_composite": 7, "build_composite_k1": 9, "composite_sketch_right_dense": 10, "composite_sketch_right_dense_nosched": 8, "sketch_right_dense": 1, "sketch_right_csr": 1,
                 "k1_schedule": 2, "sketch_right_dense_sched": 1,
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 6,

@@ -313,3 +313,38 @@ extern "C" int srlu_build_composite_k1(uint64_t seed, int64_t k, int64_t l, int6
     if (rc != SRLU_OK || sched == nullptr) return rc;
     return srlu_k1_schedule(sorted, bucket_ptr, n, l, *pad, dtype, sched, sched_bytes, stream);
 }
+
+extern "C" int srlu_sketch_right_dense_sched(const void *a, int dtype, int64_t m, int64_t n,
+                                             int64_t lda, const void *sched, size_t sched_bytes,
+                                             int64_t l1, const double *phase1, const int32_t *idx1,
+                                             int64_t k1, int64_t pad1, double mult1, double *y,
+                                             int64_t ldy, int *nonfinite, srlu_stream_t stream);
+extern "C" int srlu_sketch_right_dense(const void *a, int dtype, int64_t m, int64_t n, int64_t lda,
+                                       const int32_t *sorted1, const int32_t *bucket_ptr1,
+                                       int64_t l1, const double *phase1, const int32_t *idx1,
+                                       int64_t k1, int64_t pad1, double mult1, double *y,
+                                       int64_t ldy, int *nonfinite, srlu_stream_t stream);
+
+// Stage 1 of an attempt (randlu.py:252 build_composite + :253 apply_sketch_right)
+// in one host entry: the composite draws, plan and K1 schedule, the
+// non-finite flag reset and the K1 launch are enqueued back to back, so the
+// sketch kernel does not wait on the caller's bookkeeping between them.
+extern "C" int srlu_composite_sketch_right_dense(
+    uint64_t seed, int64_t k, int64_t l, int64_t n, int32_t *row_of, double *sign,
+    int32_t *sorted, int32_t *bucket_ptr, double *phase, int32_t *sample_idx, int64_t *pad,
+    void *staging, size_t staging_bytes, void *ws, size_t ws_bytes, void *sched,
+    size_t sched_bytes, const void *a, int dtype, int64_t m, int64_t lda, double mult, double *y,
+    int64_t ldy, int *nonfinite, srlu_stream_t stream) {
+    SRLU_REQUIRE(a != nullptr && y != nullptr && nonfinite != nullptr, SRLU_ERR_ARG,
+                 "composite_sketch_right_dense: null A, Y or flag");
+    int rc = srlu_build_composite_k1(seed, k, l, n, row_of, sign, sorted, bucket_ptr, phase,
+                                     sample_idx, pad, staging, staging_bytes, ws, ws_bytes, dtype,
+                                     sched, sched_bytes, stream);
+    if (rc != SRLU_OK) return rc;
+    SRLU_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), (cudaStream_t)stream));
+    if (sched != nullptr)
+        return srlu_sketch_right_dense_sched(a, dtype, m, n, lda, sched, sched_bytes, l, phase,
+                                             sample_idx, k, *pad, mult, y, ldy, nonfinite, stream);
+    return srlu_sketch_right_dense(a, dtype, m, n, lda, sorted, bucket_ptr, l, phase, sample_idx, k,
+                                   *pad, mult, y, ldy, nonfinite, stream);
+}

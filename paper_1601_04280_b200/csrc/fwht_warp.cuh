@@ -144,11 +144,12 @@ __device__ __forceinline__ void fwht_block_warp_dyn512(double *blk, int pad, int
 // transformed in place.  Only the NB-1 butterfly nodes feeding that output
 // are formed, level by level (stage h = bsize first), with exactly the
 // operands and order of the full network (bit-identical).
+// Blocks b >= nzb are all-zero and not stored (x + 0 and 0 +- x are exact).
 template <int NB>
-__device__ __forceinline__ double wht_pick(const double *row, int bsize, int o, int B) {
+__device__ __forceinline__ double wht_pick(const double *row, int bsize, int o, int B, int nzb = NB) {
     double u[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) u[b] = row[b * bsize + o];
+    for (int b = 0; b < NB; ++b) u[b] = b < nzb ? row[b * bsize + o] : 0.0;
 #pragma unroll
     for (int s = 1, lvl = 0; s < NB; s <<= 1, ++lvl) {
         const double sg = pm_one((B >> lvl) & 1);

@@ -43,14 +43,15 @@ namespace k1s {
 
 constexpr int kGW = 28;                 // gather warps (of 32)
 constexpr int kNT = 1024;
-constexpr int kMaxChunks = 4;
+constexpr int kMaxChunks = 4;          // codes staged in shared memory
+constexpr int kMaxChunksG = 32;        // codes read from global memory (L2-resident)
 constexpr int kMaxStages = 8;
 constexpr int kZeroBytes = 128;         // zero tail per staged row: one word per bank
 constexpr size_t kSmemMax = 232448 - 1024;
 constexpr int kHeader = 16;             // int32 header words
 
 struct Cfg {
-    int es, rb, bpt, c, nch, ns, ng, zpad, d2, sorted, joint;
+    int es, rb, bpt, c, nch, ns, ng, zpad, d2, sorted, joint, xpad;
     int64_t stage_bytes, row_stride, xs_bytes, code_cap, smem;
     // workspace offsets (bytes)
     int64_t off_grp, off_np, off_wsched, off_codes, ws_bytes;
@@ -70,7 +71,7 @@ static bool config_try(int64_t n, int64_t l, int64_t pad, int es, int bpt, int r
     cmax &= ~31LL;
     if (cmax < 32) return false;
     int64_t nch = ceil_div(n, cmax);
-    if (nch > kMaxChunks) return false;
+    if (nch > kMaxChunksG) return false;
     int64_t c = ((ceil_div(n, nch) + 31) / 32) * 32;
     if (c + kZeroBytes / es > 32767) return false;
     Cfg f{};
@@ -85,9 +86,17 @@ static bool config_try(int64_t n, int64_t l, int64_t pad, int es, int bpt, int r
     f.joint = env_int("SRLU_K1_JOINT", f.sorted ? 0 : 1) != 0;  // testing knob
     f.row_stride = (c + f.zpad) * es;
     f.stage_bytes = rb * f.row_stride;
-    f.xs_bytes = 2LL * rb * pad * 8;
-    // leave room for the codes (~64 B per warp step, ~n/16 steps)
-    const int64_t code_est = env_int("SRLU_K1_GCODES", 0) ? 0 : 4 * n + 4096;
+    // FWHT scratch: only the bsize-point blocks that hold buckets (blocks
+    // past ceil(l / bsize) stay zero through the in-block stages and enter
+    // the output-pruned cross-block stages as zeros)
+    {
+        const int64_t bs = pad < 512 ? pad : 512;
+        f.xpad = (int)(ceil_div(l, bs) * bs);
+    }
+    f.xs_bytes = 2LL * rb * f.xpad * 8;
+    // leave room for the codes (~64 B per warp step, ~n/16 steps); more than
+    // kMaxChunks chunks: the codes stay in global memory
+    const int64_t code_est = (env_int("SRLU_K1_GCODES", 0) || nch > kMaxChunks) ? 0 : 4 * n + 4096;
     int ns = env_int("SRLU_K1_NS", 4);
     if (ns < 2) ns = 2;
     if (ns > kMaxStages) ns = kMaxStages;
@@ -120,7 +129,7 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     if (pad < 32 || pad > 8192 || l < 1 || l > pad || n < 1) return false;
     const int64_t groups = ceil_div(l, 32);
     int bpt = 0;
-    for (int b : {1, 2, 4})
+    for (int b : {1, 2, 4, 5, 8})
         if ((int64_t)kGW * b >= groups) { bpt = b; break; }
     if (!bpt) return false;
     const int64_t row_bytes = n * es;
@@ -133,8 +142,11 @@ static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
     }
     for (int rb = row_bytes <= 8192 ? 4 : 2; rb >= 1; rb >>= 1)
         for (int64_t st = 65536; st >= 16384; st >>= 1)
-            if (config_try(n, l, pad, es, bpt, rb, st, cf)) return true;
-    return false;
+            if (config_try(n, l, pad, es, bpt, rb, st, cf) && cf->nch <= kMaxChunks) return true;
+    // long rows (codes read from L2): one row per block, the widest chunks
+    // (fewest idle lane-steps per chunk; measured at config 5: 64 KB stages
+    // 13.9 ms, 32 KB 24 ms, 16 KB 43 ms, two-row blocks of 2048 columns 32 ms)
+    return config_try(n, l, pad, es, bpt, 1, 65536, cf);
 }
 
 // warp w, slot b -> group (snake order over the slots)
@@ -366,7 +378,7 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
 // the sketch kernel
 
 struct Dev {
-    int c, nch, ns, ng, dbg, pf, sorted, joint;
+    int c, nch, ns, ng, dbg, pf, sorted, joint, xpad;
     int row_stride, stage_bytes;
     int xs_off, code_off, code_cap;
 };
@@ -418,7 +430,7 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
                                             const double *__restrict__ phase, const Dev &d,
                                             int64_t my_nrb, int64_t nitems, uint64_t *full,
                                             uint64_t *xs_full, uint64_t *xs_empty, unsigned *rel,
-                                            double *xs_base, int pad, int l, const Issue &issue) {
+                                            double *xs_base, int xpad, int l, const Issue &issue) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int bt[BPT];
     bool bneg[BPT];
@@ -485,8 +497,12 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
             }
         }
         const int buf = (int)(rbi & 1);
-        if (rbi >= 2) mbar_wait_sleep(&xs_empty[buf], (unsigned)(((rbi >> 1) - 1) & 1), 256);
-        double *xs = xs_base + (size_t)buf * RB * pad;
+        if (rbi >= 2) {
+            const unsigned par = (unsigned)(((rbi >> 1) - 1) & 1);
+            if (d.dbg & 32) mbar_wait_sleep(&xs_empty[buf], par, 256);
+            else mbar_wait_suspend(&xs_empty[buf], par);
+        }
+        double *xs = xs_base + (size_t)buf * RB * xpad;
         // +-phase, scatter by bucket, then (after all gather warps wrote) the
         // FWHT stages h < 32 by shuffles on 32-aligned blocks of buckets;
         // positions >= l (no bucket) enter as zeros
@@ -497,7 +513,7 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
                     const int pos = fwht_sw(bt[b]);
 #pragma unroll
                     for (int r = 0; r < RB; ++r)
-                        xs[r * pad + pos] = bneg[b] ? -acc[b][r] : acc[b][r];
+                        xs[r * xpad + pos] = bneg[b] ? -acc[b][r] : acc[b][r];
                 }
             }
             named_bar(2, kGW * 32);
@@ -506,7 +522,7 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
                 const bool live = q * 32 + lane < l;
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
-                    xs[r * pad + pos] = fwht_lane_stages(live ? xs[r * pad + pos] : 0.0, lane);
+                    xs[r * xpad + pos] = fwht_lane_stages(live ? xs[r * xpad + pos] : 0.0, lane);
             }
         } else {
             // consecutive buckets: slot g*32 + lane holds bucket g*32 + lane
@@ -517,7 +533,7 @@ __device__ __forceinline__ void gather_warp(unsigned char *smem, Codes cw,
 #pragma unroll
                 for (int r = 0; r < RB; ++r) {
                     const double v = fwht_lane_stages(bneg[b] ? -acc[b][r] : acc[b][r], lane);
-                    if (g * 32 < pad) xs[r * pad + pos] = v;
+                    if (g * 32 < xpad) xs[r * xpad + pos] = v;
                 }
             }
         }
@@ -565,7 +581,8 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
             reinterpret_cast<uint32_t *>(smem + (size_t)sr * d.row_stride + (size_t)d.c * es)[w] = 0u;
         }
     }
-    for (int i = tid; i < 2 * RB * pad; i += kNT) xs_base[i] = 0.0;
+    const int xpad = d.xpad;
+    for (int i = tid; i < 2 * RB * xpad; i += kNT) xs_base[i] = 0.0;
     if (codes_in_smem) {
         const uint4 *src = reinterpret_cast<const uint4 *>(codes_g);
         uint4 *dst = reinterpret_cast<uint4 *>(codes_s);
@@ -613,10 +630,10 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
     if (warp < kGW) {
         if (codes_in_smem)
             gather_warp<T, RB, BPT>(smem, codes_s, grp, wsched, phase, d, my_nrb, nitems, full,
-                                    xs_full, xs_empty, rel, xs_base, pad, l, issue);
+                                    xs_full, xs_empty, rel, xs_base, xpad, l, issue);
         else
             gather_warp<T, RB, BPT>(smem, codes_g, grp, wsched, phase, d, my_nrb, nitems, full,
-                                    xs_full, xs_empty, rel, xs_base, pad, l, issue);
+                                    xs_full, xs_empty, rel, xs_base, xpad, l, issue);
         return;
     }
     // ---------------------------------------------------------------- epilogue
@@ -628,12 +645,13 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
     bool bad = false;
     for (int64_t rbi = 0; rbi < my_nrb; ++rbi) {
         const int buf = (int)(rbi & 1);
-        mbar_wait_sleep(&xs_full[buf], (unsigned)((rbi >> 1) & 1), 32);
-        double *xs = xs_base + (size_t)buf * RB * pad;
+        if (d.dbg & 32) mbar_wait_sleep(&xs_full[buf], (unsigned)((rbi >> 1) & 1), 32);
+        else mbar_wait_suspend(&xs_full[buf], (unsigned)((rbi >> 1) & 1));
+        double *xs = xs_base + (size_t)buf * RB * xpad;
         // stages 32 <= h < bsize (the gather warps applied h < 32)
         for (int item = ew; !(d.dbg & 1) && item < RB * nzb; item += kEW) {
             const int r = item / nzb, bb = item % nzb;
-            fwht_block_warp_hi_dyn512(xs + (size_t)r * pad + (size_t)bb * bsize, bsize, lane);
+            fwht_block_warp_hi_dyn512(xs + (size_t)r * xpad + (size_t)bb * bsize, bsize, lane);
         }
         named_bar(1, kEW * 32);
         // output-pruned stages h >= bsize for the k sampled outputs only
@@ -645,14 +663,14 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
                 if (r < nrows) {
-                    const double *row = xs + (size_t)r * pad;
+                    const double *row = xs + (size_t)r * xpad;
                     double f;
                     switch (nb) {
                         case 1: f = row[o]; break;
-                        case 2: f = wht_pick<2>(row, bsize, o, B); break;
-                        case 4: f = wht_pick<4>(row, bsize, o, B); break;
-                        case 8: f = wht_pick<8>(row, bsize, o, B); break;
-                        default: f = wht_pick<16>(row, bsize, o, B); break;
+                        case 2: f = wht_pick<2>(row, bsize, o, B, nzb); break;
+                        case 4: f = wht_pick<4>(row, bsize, o, B, nzb); break;
+                        case 8: f = wht_pick<8>(row, bsize, o, B, nzb); break;
+                        default: f = wht_pick<16>(row, bsize, o, B, nzb); break;
                     }
                     const double v = __dmul_rn(f, mult);
                     y[(row0 + r) * ldy + kk] = v;
@@ -666,7 +684,7 @@ __global__ void __launch_bounds__(kNT, 1) k1s_kernel(
         const int z0 = d.sorted ? (l + 31) / 32 * 32 : d.ng * 32, z1 = nzb * bsize;
         for (int i = etid; z1 > z0 && i < RB * (z1 - z0); i += kEW * 32) {
             const int r = i / (z1 - z0), t = z0 + i % (z1 - z0);
-            xs[(size_t)r * pad + fwht_sw(t)] = 0.0;
+            xs[(size_t)r * xpad + fwht_sw(t)] = 0.0;
         }
         mbar_arrive(&xs_empty[buf]);
     }
@@ -680,9 +698,9 @@ static int launch(const Cfg &f, const T *a, int64_t m, int64_t n, int64_t lda,
                   cudaStream_t s) {
     Dev d;
     d.c = f.c; d.nch = f.nch; d.ns = f.ns; d.ng = f.ng;
-    d.sorted = f.sorted; d.joint = f.joint;
+    d.sorted = f.sorted; d.joint = f.joint; d.xpad = f.xpad;
     d.pf = env_int("SRLU_K1_PF", 0);  // L2 prefetch distance in ring items (measured: no gain)
-    d.dbg = env_int("SRLU_K1_DBG", 0);  // experiments: 1 no FWHT, 2 no outputs, 8 no waits
+    d.dbg = env_int("SRLU_K1_DBG", 0);  // experiments: 1 no FWHT, 2 no outputs, 8 no waits, 32 sleep-polling hand-off waits
     d.row_stride = (int)f.row_stride; d.stage_bytes = (int)f.stage_bytes;
     d.xs_off = (int)(f.ns * f.stage_bytes);
     d.code_off = (int)(d.xs_off + f.xs_bytes);
@@ -713,6 +731,7 @@ static int dispatch(const Cfg &f, const T *a, int64_t m, int64_t n, int64_t lda,
     K1S_CASE(1, 1) K1S_CASE(1, 2) K1S_CASE(1, 4)
     K1S_CASE(2, 1) K1S_CASE(2, 2) K1S_CASE(2, 4)
     K1S_CASE(4, 1) K1S_CASE(4, 2) K1S_CASE(4, 4)
+    K1S_CASE(1, 5) K1S_CASE(2, 5) K1S_CASE(1, 8) K1S_CASE(2, 8)
 #undef K1S_CASE
     set_error("sketch_right_dense_sched: no kernel for rb=%d bpt=%d", f.rb, f.bpt);
     return SRLU_ERR_UNSUPPORTED;

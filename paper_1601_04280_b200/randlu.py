@@ -31,8 +31,8 @@ from .errors import DecompositionError, ParameterError, ShapeError, SingularMatr
 from .factor import check_rank, dgemm, lu_col_pivot_dev, lu_row_pivot_dev, pinv_dev
 from .matrix import COMPLEX, REAL, Matrix, Permutation
 from . import _lib
-from .sketch import (HADAMARD, build_composite, members, sketch_left_into, sketch_right_into,
-                     transform_kind_for_field)
+from .sketch import (HADAMARD, build_composite, composite_sketch_right, members,
+                     sketch_left_into, sketch_right_into, transform_kind_for_field)
 
 logger = logging.getLogger(__name__)
 
@@ -306,12 +306,14 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     ev = _stage_events(dev, len(STAGES) + 1)
     ev[0].record(main)
 
-    k1_dtype = None if a.is_sparse else _lib.dtype_code(a.raw.dtype)
-    om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev,
-                          k1_dtype=k1_dtype)
     y = torch.empty(m, k1, dtype=torch.float64, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    sketch_right_into(a, om1, y, flag)
+    if a.is_sparse:
+        om1 = build_composite(k1, params.l1, n, kind, params.seed + 2 * attempt, dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        sketch_right_into(a, om1, y, flag)
+    else:  # draws, plan, schedule and K1 in one C call
+        flag = torch.empty(1, dtype=torch.int32, device=dev)
+        om1 = composite_sketch_right(a, k1, params.l1, kind, params.seed + 2 * attempt, y, flag)
     ev[1].record(main)
     # Omega2 (draws + plan + member table of L1) on the side stream while K1
     # runs (independent of everything enqueued so far)

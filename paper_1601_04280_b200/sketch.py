@@ -259,6 +259,26 @@ def build_composite(k, l, n, kind, seed, device=None, stream=None, k1_dtype=None
     draws -> pinned staging -> upload, all enqueued on `stream`; with
     ``k1_dtype`` (an A element-type code) also the scheduled K1's gather
     schedule.  The device work is enqueued before the Python bookkeeping."""
+    return _composite(k, l, n, kind, seed, device, stream, k1_dtype, None)
+
+
+def composite_sketch_right(a: Matrix, k, l, kind, seed, y: torch.Tensor, nonfinite: torch.Tensor,
+                           stream=None) -> CompositeSketch:
+    """Stage 1 of an attempt for a dense A (randlu.py:252-253): build_composite
+    (k x n, `seed`) and y = A · omega^* with nonfinite reset to 0 first, in ONE
+    C call (srlu_composite_sketch_right_dense) so that K1 is enqueued right
+    behind the draws and its schedule; the Python bookkeeping of the sketch
+    object runs while K1 streams A."""
+    t = a.raw
+    n = a.cols
+    es = t.element_size()
+    aligned = t.data_ptr() % 16 == 0 and (t.stride(0) * es) % 16 == 0 and (n * es) % 16 == 0
+    k1_dtype = _lib.dtype_code(t.dtype)
+    return _composite(k, l, n, kind, seed, t.device, stream, k1_dtype if aligned else None,
+                      (t, k1_dtype, y, nonfinite))
+
+
+def _composite(k, l, n, kind, seed, device, stream, k1_dtype, right):
     if kind not in (FOURIER, HADAMARD):
         raise ParameterError(f"unknown transform kind {kind!r}")
     if kind == FOURIER:
@@ -278,13 +298,26 @@ def build_composite(k, l, n, kind, seed, device=None, stream=None, k1_dtype=None
     padc = ctypes.c_int64(0)
     sh = _lib.stream_handle(stream)
     P_ = ctypes.c_void_p
-    _lib.check(L.srlu_build_composite_k1(
-        seed, k, l, n, P_(base + off["row"]), P_(base + off["sign"]), P_(base + off["sorted"]),
-        P_(base + off["bptr"]), P_(base + off["phase"]), P_(base + off["idx"]),
-        ctypes.addressof(padc), staging.data_ptr(), staging.numel(), P_(base + off["ws"]),
-        ws_bytes, -1 if k1_dtype is None else k1_dtype,
-        P_(base + off["sched"]) if sched_bytes else None, sched_bytes, sh),
-        "build_composite_k1" if sched_bytes else "build_composite")
+    if right is None:
+        _lib.check(L.srlu_build_composite_k1(
+            seed, k, l, n, P_(base + off["row"]), P_(base + off["sign"]), P_(base + off["sorted"]),
+            P_(base + off["bptr"]), P_(base + off["phase"]), P_(base + off["idx"]),
+            ctypes.addressof(padc), staging.data_ptr(), staging.numel(), P_(base + off["ws"]),
+            ws_bytes, -1 if k1_dtype is None else k1_dtype,
+            P_(base + off["sched"]) if sched_bytes else None, sched_bytes, sh),
+            "build_composite_k1" if sched_bytes else "build_composite")
+    else:
+        t, dcode, y, nonfinite = right
+        m = t.shape[0]
+        _lib.check(L.srlu_composite_sketch_right_dense(
+            seed, k, l, n, P_(base + off["row"]), P_(base + off["sign"]), P_(base + off["sorted"]),
+            P_(base + off["bptr"]), P_(base + off["phase"]), P_(base + off["idx"]),
+            ctypes.addressof(padc), staging.data_ptr(), staging.numel(), P_(base + off["ws"]),
+            ws_bytes, P_(base + off["sched"]) if sched_bytes else None, sched_bytes,
+            P_(t.data_ptr()), dcode, m, t.stride(0), math.sqrt(pad / k) / math.sqrt(pad),
+            P_(y.data_ptr()),
+            y.stride(0), P_(nonfinite.data_ptr()), sh),
+            "composite_sketch_right_dense" if sched_bytes else "composite_sketch_right_dense_nosched")
     _STAGING.put(staging, stream if stream is not None else torch.cuda.current_stream(dev))
     assert padc.value == pad
     isz = {torch.float64: 8, torch.int32: 4}

@@ -2,7 +2,7 @@
 CPU oracle: Y = A · Omega1^* must be bit-identical to the reference's
 sem_gather_dense + fast_adjoint_right (sketch.py:362-368; _fast.pyx:23-54)
 for every staging geometry the kernel picks (rows per block 1/2/4, one to
-four column chunks, 1/2/4 buckets per lane, fp32 and fp64 A, ragged m).
+32 column chunks, 1/2/4/5/8 buckets per lane, fp32 and fp64 A, ragged m).
 Inputs span 40 decades so that any change of the per-bucket summation order
 shows up in the last bits."""
 
@@ -37,6 +37,10 @@ SHAPES = [
     (64, 30000, np.float32, 3000, 100),   # 4 chunks, 4 buckets per lane
     (100, 12000, np.float64, 700, 64),    # fp64, 3 chunks
     (3, 4096, np.float32, 64, 16),        # fewer row blocks than SMs
+    (24, 65536, np.float64, 4400, 550),   # config-5 shape: 5 buckets per lane, > 4 chunks
+                                          # (codes in global memory), 9 of 16 FWHT blocks stored
+    (40, 50000, np.float32, 1000, 90),    # fp32 rows over 4 chunks: codes in global memory
+    (9, 20000, np.float64, 6000, 80),     # 8 buckets per lane
 ]
 
 
