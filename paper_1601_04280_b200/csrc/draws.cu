@@ -266,35 +266,56 @@ extern "C" size_t srlu_build_composite_staging(int64_t k, int64_t l) {
     return sizeof(double) * (size_t)l + sizeof(int64_t) * (size_t)k + sizeof(int32_t) * (size_t)k + 64;
 }
 
+// device half: sparse-stage draws and the accumulation plan
+static int composite_device(uint64_t seed, int64_t l, int64_t n, int32_t *row_of, double *sign,
+                            int32_t *sorted, int32_t *bucket_ptr, void *ws, size_t ws_bytes,
+                            srlu_stream_t stream) {
+    SRLU_REQUIRE(ws_bytes >= srlu_build_composite_workspace(n, l), SRLU_ERR_WORKSPACE,
+                 "build_composite: workspace too small");
+    char *w = (char *)ws;
+    const size_t ws_sem = align256(srlu_draw_sem_workspace(n, l));
+    int rc = srlu_draw_sem(seed, l, n, row_of, sign, w, ws_sem, stream);
+    if (rc != SRLU_OK) return rc;
+    return srlu_sem_plan(row_of, sign, n, l, sorted, bucket_ptr, w + ws_sem, ws_bytes - ws_sem,
+                         stream);
+}
+
+// host half: the transform stage (seed + 2**32, sketch.py:36, :276) drawn
+// sequentially like numpy into the pinned staging buffer, uploaded in one
+// copy.  Staging layout: phase[l] f64 | idx32[k] | idx64[k]; when phase and
+// sample_idx are adjacent on the device (sample_idx == phase + l) both go up
+// in a single copy.
+static int composite_host(uint64_t seed, int64_t k, int64_t l, double *phase, int32_t *sample_idx,
+                          int64_t *pad, void *staging, size_t staging_bytes, srlu_stream_t stream) {
+    SRLU_REQUIRE(staging_bytes >= srlu_build_composite_staging(k, l), SRLU_ERR_WORKSPACE,
+                 "build_composite: staging too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    double *ph = (double *)staging;
+    int32_t *idx32 = (int32_t *)(ph + l);
+    int64_t *idx64 = (int64_t *)(((uintptr_t)(idx32 + k) + 7) & ~(uintptr_t)7);
+    int rc = srlu_draw_fast_transform(seed + (1ULL << 32), k, l, ph, idx64, pad);
+    if (rc != SRLU_OK) return rc;
+    for (int64_t i = 0; i < k; ++i) idx32[i] = (int32_t)idx64[i];
+    if ((void *)sample_idx == (void *)(phase + l)) {
+        SRLU_CUDA(cudaMemcpyAsync(phase, ph, sizeof(double) * (size_t)l + sizeof(int32_t) * (size_t)k,
+                                  cudaMemcpyHostToDevice, s));
+    } else {
+        SRLU_CUDA(cudaMemcpyAsync(phase, ph, sizeof(double) * (size_t)l, cudaMemcpyHostToDevice, s));
+        SRLU_CUDA(cudaMemcpyAsync(sample_idx, idx32, sizeof(int32_t) * (size_t)k,
+                                  cudaMemcpyHostToDevice, s));
+    }
+    return SRLU_OK;
+}
+
 extern "C" int srlu_build_composite(uint64_t seed, int64_t k, int64_t l, int64_t n, int32_t *row_of,
                                     double *sign, int32_t *sorted, int32_t *bucket_ptr,
                                     double *phase, int32_t *sample_idx, int64_t *pad,
                                     void *staging, size_t staging_bytes, void *ws, size_t ws_bytes,
                                     srlu_stream_t stream) {
-    SRLU_REQUIRE(staging_bytes >= srlu_build_composite_staging(k, l), SRLU_ERR_WORKSPACE,
-                 "build_composite: staging too small");
-    SRLU_REQUIRE(ws_bytes >= srlu_build_composite_workspace(n, l), SRLU_ERR_WORKSPACE,
-                 "build_composite: workspace too small");
-    cudaStream_t s = (cudaStream_t)stream;
     // device work first (the GPU starts while the host draws the transform)
-    char *w = (char *)ws;
-    const size_t ws_sem = align256(srlu_draw_sem_workspace(n, l));
-    int rc = srlu_draw_sem(seed, l, n, row_of, sign, w, ws_sem, stream);
+    int rc = composite_device(seed, l, n, row_of, sign, sorted, bucket_ptr, ws, ws_bytes, stream);
     if (rc != SRLU_OK) return rc;
-    rc = srlu_sem_plan(row_of, sign, n, l, sorted, bucket_ptr, w + ws_sem, ws_bytes - ws_sem,
-                       stream);
-    if (rc != SRLU_OK) return rc;
-    double *ph = (double *)staging;
-    int64_t *idx64 = (int64_t *)(ph + l);
-    int32_t *idx32 = (int32_t *)(idx64 + k);
-    // transform stage: seed + 2**32 (sketch.py:36, :276)
-    rc = srlu_draw_fast_transform(seed + (1ULL << 32), k, l, ph, idx64, pad);
-    if (rc != SRLU_OK) return rc;
-    for (int64_t i = 0; i < k; ++i) idx32[i] = (int32_t)idx64[i];
-    SRLU_CUDA(cudaMemcpyAsync(phase, ph, sizeof(double) * (size_t)l, cudaMemcpyHostToDevice, s));
-    SRLU_CUDA(cudaMemcpyAsync(sample_idx, idx32, sizeof(int32_t) * (size_t)k,
-                              cudaMemcpyHostToDevice, s));
-    return SRLU_OK;
+    return composite_host(seed, k, l, phase, sample_idx, pad, staging, staging_bytes, stream);
 }
 
 extern "C" size_t srlu_k1_schedule_bytes(int64_t n, int64_t l1, int64_t pad1, int dtype);
@@ -308,10 +329,17 @@ extern "C" int srlu_build_composite_k1(uint64_t seed, int64_t k, int64_t l, int6
                                        int64_t *pad, void *staging, size_t staging_bytes, void *ws,
                                        size_t ws_bytes, int dtype, void *sched, size_t sched_bytes,
                                        srlu_stream_t stream) {
-    int rc = srlu_build_composite(seed, k, l, n, row_of, sign, sorted, bucket_ptr, phase,
-                                  sample_idx, pad, staging, staging_bytes, ws, ws_bytes, stream);
-    if (rc != SRLU_OK || sched == nullptr) return rc;
-    return srlu_k1_schedule(sorted, bucket_ptr, n, l, *pad, dtype, sched, sched_bytes, stream);
+    // device draws, plan and the K1 schedule (which needs only the plan) are
+    // all enqueued before the host draws the transform stage
+    int rc = composite_device(seed, l, n, row_of, sign, sorted, bucket_ptr, ws, ws_bytes, stream);
+    if (rc != SRLU_OK) return rc;
+    if (sched != nullptr) {
+        int64_t pad1 = 1;
+        while (pad1 < l) pad1 <<= 1;
+        rc = srlu_k1_schedule(sorted, bucket_ptr, n, l, pad1, dtype, sched, sched_bytes, stream);
+        if (rc != SRLU_OK) return rc;
+    }
+    return composite_host(seed, k, l, phase, sample_idx, pad, staging, staging_bytes, stream);
 }
 
 extern "C" int srlu_sketch_right_dense_sched(const void *a, int dtype, int64_t m, int64_t n,

@@ -236,12 +236,13 @@ def _composite_layout(L, k, l, n, k1_dtype):
     lay = _LAYOUTS.get(key)
     if lay is None:
         i4 = lambda c: ((c * 4 + 7) // 8) * 8
+        # phase and idx adjacent: the C side uploads both in one copy
         off = {"sign": 0, "phase": n * 8}
-        off["row"] = off["phase"] + l * 8
+        off["idx"] = off["phase"] + l * 8
+        off["row"] = off["idx"] + i4(k)
         off["sorted"] = off["row"] + i4(n)
         off["bptr"] = off["sorted"] + i4(n)
-        off["idx"] = off["bptr"] + i4(l + 1)
-        off["ws"] = ((off["idx"] + i4(k)) + 255) // 256 * 256
+        off["ws"] = ((off["bptr"] + i4(l + 1)) + 255) // 256 * 256
         ws_bytes = L.srlu_build_composite_workspace(n, l)
         sched_bytes = 0
         if k1_dtype is not None:
