@@ -17,6 +17,8 @@
 //    and L products (cuBLAS picks a 32x32 DMMA tile that reached <3 TFLOP/s
 //    on the 16384x118x110 shape).
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -598,6 +600,282 @@ using namespace srlu;
 
 extern "C" size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2) { return qr_pinv_smem(k1, k2); }
 
+// Lookahead variant (k1 * TPC + 32 <= 1024): warp 0 runs the critical
+// chain alone — for column c it applies reflector c-1 and forms reflector c
+// (32 lanes on one column, warp-level sums) — while the group of TPC
+// threads that owns column c applies reflectors 0..c-2 in the background
+// and then hands the column to warp 0 (mbarrier rdy[c]).  In qr_kernel the
+// critical column's group shares its warp with three other columns'
+// groups (divergent paths issue one at a time) and its scheduler with
+// every spinning waiter; here the chain has a warp of its own and the
+// background waits suspend.  Same reflector conventions as qr_kernel.
+template <int TPC>
+__global__ void __launch_bounds__(1024, 1) qr_la_kernel(const double *__restrict__ mT, int k1,
+                                                        int k2, int64_t ldm,
+                                                        double *__restrict__ qa,
+                                                        double *__restrict__ qtau,
+                                                        double *__restrict__ rrow, int depth) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ld = k2 | 1;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);           // k1: reflector formed
+    double *s_tau = reinterpret_cast<double *>(smem_raw) + k1;        // k1
+    double *s_scal = s_tau + k1;                                      // k1
+    double *A = s_scal + k1;                                          // column c: A[c*ld + r]
+    uint64_t *rdy = reinterpret_cast<uint64_t *>(A + (size_t)k1 * ld);  // k1: background done
+    const int tid = threadIdx.x;
+    {
+        const int n = k1 * k2;
+        for (int i0 = tid; i0 < n; i0 += 8 * blockDim.x) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                v[u] = i < n ? mT[(int64_t)(i / k2) * ldm + i % k2] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < n) A[(i / k2) * ld + i % k2] = v[u];
+            }
+        }
+    }
+    for (int i = tid; i < k1; i += blockDim.x) {
+        mbar_init(bar + i, 32);
+        mbar_init(rdy + i, TPC);
+    }
+    __syncthreads();
+
+    if (tid < 32) {
+        // ---- the critical chain ----
+        const int lane = tid;
+        for (int c = 0; c < k1; ++c) {
+            double *colc = A + (size_t)c * ld;
+            double p0 = 0.0, p1 = 0.0;
+            if (c > 0) mbar_wait(rdy + c, 0);
+            // reflectors c-depth .. c-2 (the background applied the earlier ones)
+            for (int j = max(0, c - depth); j + 1 < c; ++j) {
+                const double tq = s_tau[j];
+                if (tq == 0.0) continue;
+                const double scal = s_scal[j];
+                const double *colj = A + (size_t)j * ld;
+                double w0 = 0.0, w1 = 0.0;
+                int r = j + 1 + lane;
+                for (; r + 32 < k2; r += 64) {
+                    w0 = __fma_rn(colj[r], colc[r], w0);
+                    w1 = __fma_rn(colj[r + 32], colc[r + 32], w1);
+                }
+                if (r < k2) w0 = __fma_rn(colj[r], colc[r], w0);
+                const double dot = group_sum<32>(w0 + w1);
+                const double f = tq * __fma_rn(scal, dot, colc[j]);
+                const double fs = f * scal;
+                __syncwarp();
+                if (lane == 0) colc[j] -= f;
+                for (r = j + 1 + lane; r < k2; r += 32) colc[r] = __fma_rn(-fs, colj[r], colc[r]);
+                __syncwarp();
+            }
+            const double tj = c > 0 ? s_tau[c - 1] : 0.0;
+            if (c > 0 && tj != 0.0) {
+                const int j = c - 1;
+                const double scal = s_scal[j];
+                const double *colj = A + (size_t)j * ld;
+                double w0 = 0.0, w1 = 0.0;
+                int r = j + 1 + lane;
+                for (; r + 32 < k2; r += 64) {
+                    w0 = __fma_rn(colj[r], colc[r], w0);
+                    w1 = __fma_rn(colj[r + 32], colc[r + 32], w1);
+                }
+                if (r < k2) w0 = __fma_rn(colj[r], colc[r], w0);
+                const double dot = group_sum<32>(w0 + w1);
+                const double f = tj * __fma_rn(scal, dot, colc[j]);
+                const double fs = f * scal;
+                __syncwarp();  // every lane has read colc[j]
+                if (lane == 0) colc[j] -= f;
+                for (r = j + 1 + lane; r < k2; r += 32) {
+                    const double nv = __fma_rn(-fs, colj[r], colc[r]);
+                    colc[r] = nv;
+                    if (r > c) {
+                        if (r & 32) p1 = __fma_rn(nv, nv, p1);
+                        else p0 = __fma_rn(nv, nv, p0);
+                    }
+                }
+            } else {
+                for (int r = c + 1 + lane; r < k2; r += 32) p0 = __fma_rn(colc[r], colc[r], p0);
+            }
+            const double part = group_sum<32>(p0 + p1);
+            __syncwarp();
+            if (lane == 0) dlarfg(colc, c, part, s_tau + c, s_scal + c);
+            __syncwarp();
+            mbar_arrive(bar + c);
+        }
+    } else {
+        // ---- background: column c gets reflectors 0..c-2 ----
+        const int g = (tid - 32) / TPC, q = (tid - 32) % TPC;
+        const unsigned gmask = (TPC == 32 ? 0xffffffffu
+                                          : ((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1)));
+        const int c = g;
+        if (c < k1) {
+            double *colc = A + (size_t)c * ld;
+            for (int j = 0; j < c - depth; ++j) {
+                mbar_wait_suspend(bar + j, 0);
+                const double tj = s_tau[j];
+                if (tj == 0.0) continue;
+                const double scal = s_scal[j];
+                const double *colj = A + (size_t)j * ld;
+                double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+                int r = j + 1 + q;
+                for (; r + 3 * TPC < k2; r += 4 * TPC) {
+                    w0 = __fma_rn(colj[r], colc[r], w0);
+                    w1 = __fma_rn(colj[r + TPC], colc[r + TPC], w1);
+                    w2 = __fma_rn(colj[r + 2 * TPC], colc[r + 2 * TPC], w2);
+                    w3 = __fma_rn(colj[r + 3 * TPC], colc[r + 3 * TPC], w3);
+                }
+                for (; r < k2; r += TPC) w0 = __fma_rn(colj[r], colc[r], w0);
+                const double dot = group_sum<TPC>((w0 + w1) + (w2 + w3));
+                const double f = tj * __fma_rn(scal, dot, colc[j]);
+                const double fs = f * scal;
+                __syncwarp(gmask);
+                if (q == 0) colc[j] -= f;
+                for (r = j + 1 + q; r < k2; r += TPC) colc[r] = __fma_rn(-fs, colj[r], colc[r]);
+            }
+            mbar_arrive(rdy + c);
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < k1; i += blockDim.x) qtau[i] = s_tau[i];
+    for (int i = tid; i < k1 * ld; i += blockDim.x) {
+        const int cc = i / ld, r = i % ld;
+        double v = A[i];
+        if (r > cc && r < k2 && s_tau[cc] != 0.0) v *= s_scal[cc];
+        qa[i] = v;
+    }
+    for (int i = tid; i < k1 * k1; i += blockDim.x) {
+        const int r = i / k1, cc = i % k1;
+        rrow[i] = r <= cc ? A[cc * ld + r] : 0.0;
+    }
+}
+
+// Register-resident variant (k2 <= 8 * RPT, k1 <= 128): the 8 threads of
+// column c's group keep its rows q, q + 8, ... in registers for the whole
+// sweep; shared memory only carries each reflector once it is formed (the
+// groups of a warp read the same reflector words: broadcast), so the
+// trailing columns no longer stream their own data through shared memory
+// and the critical chain (apply reflector c-1, form reflector c) competes
+// for far fewer shared-memory cycles.  Same dataflow and dlarfg
+// conventions as qr_kernel (not the same summation order: the QR is
+// compared with LAPACK's to tolerance anyway).
+template <int RPT>
+__device__ __forceinline__ double pick_reg(const double (&v)[RPT], int idx) {
+    double x = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) x = (i == idx) ? v[i] : x;
+    return x;
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(1024, 1) qr_reg_kernel(const double *__restrict__ mT, int k1,
+                                                         int k2, int64_t ldm,
+                                                         double *__restrict__ qa,
+                                                         double *__restrict__ qtau,
+                                                         double *__restrict__ rrow) {
+    constexpr int TPC = 8;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ld = k2 | 1;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);           // k1 mbarriers
+    double *s_tau = reinterpret_cast<double *>(smem_raw) + k1;        // k1
+    double *s_scal = s_tau + k1;                                      // k1
+    double *A = s_scal + k1;  // column c: A[c*ld + r] (reflectors, then the result)
+    const int tid = threadIdx.x;
+    const int c = tid / TPC, q = tid % TPC;
+    const unsigned gmask = ((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1));
+    for (int i = tid; i < k1; i += blockDim.x) mbar_init(bar + i, TPC);
+    double v[RPT];
+    if (c < k1) {
+        const double *src = mT + (int64_t)c * ldm;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = q + TPC * i;
+            v[i] = r < k2 ? __ldg(src + r) : 0.0;
+        }
+    }
+    __syncthreads();
+    if (c < k1) {
+        // element of row rr: lane rr % TPC of the group, register rr / TPC
+#define QR_ROW_VAL(out, rr) \
+    out = __shfl_sync(gmask, pick_reg<RPT>(v, (rr) / TPC), (tid & 31 & ~(TPC - 1)) + (rr) % TPC)
+        for (int j = 0; j < c; ++j) {
+            mbar_wait(bar + j, 0);
+            const double tj = s_tau[j];
+            if (tj == 0.0) continue;
+            const double scal = s_scal[j];
+            const double *colj = A + (size_t)j * ld;
+            double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = q + TPC * i;
+                if (r > j && r < k2) {
+                    if (i & 1) w1 = __fma_rn(colj[r], v[i], w1);
+                    else w0 = __fma_rn(colj[r], v[i], w0);
+                }
+            }
+            const double dot = group_sum<TPC>(w0 + w1);
+            double vj;
+            QR_ROW_VAL(vj, j);
+            const double f = tj * __fma_rn(scal, dot, vj);
+            const double fs = f * scal;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = q + TPC * i;
+                if (r == j) v[i] -= f;
+                else if (r > j && r < k2) v[i] = __fma_rn(-fs, colj[r], v[i]);
+            }
+        }
+        // reflector c from rows > c, alpha = row c
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = q + TPC * i;
+            if (r > c && r < k2) {
+                if (i & 1) p1 = __fma_rn(v[i], v[i], p1);
+                else p0 = __fma_rn(v[i], v[i], p0);
+            }
+        }
+        const double part = group_sum<TPC>(p0 + p1);
+        double alpha;
+        QR_ROW_VAL(alpha, c);
+#undef QR_ROW_VAL
+        double t = 0.0, scal = 0.0, beta = alpha;
+        if (part > 0.0) {
+            beta = -copysign(sqrt(__fma_rn(alpha, alpha, part)), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        double *colc = A + (size_t)c * ld;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = q + TPC * i;
+            if (r == c) v[i] = beta;
+            if (r < k2) colc[r] = v[i];  // rows < c: R (final); > c: the reflector
+        }
+        if (q == 0) {
+            s_tau[c] = t;
+            s_scal[c] = scal;
+        }
+        mbar_arrive(bar + c);
+    }
+    __syncthreads();
+    for (int i = tid; i < k1; i += blockDim.x) qtau[i] = s_tau[i];
+    for (int i = tid; i < k1 * ld; i += blockDim.x) {
+        const int cc = i / ld, r = i % ld;
+        double x = A[i];
+        if (r > cc && r < k2 && s_tau[cc] != 0.0) x *= s_scal[cc];
+        qa[i] = x;
+    }
+    for (int i = tid; i < k1 * k1; i += blockDim.x) {
+        const int r = i / k1, cc = i % k1;
+        rrow[i] = r <= cc ? A[cc * ld + r] : 0.0;
+    }
+}
+
 extern "C" size_t srlu_qr_pinv_workspace(int64_t k1, int64_t k2) {
     return sizeof(double) * (size_t)(k1 * (k2 | 1) + k1 + k1 * k1) + 256;
 }
@@ -618,11 +896,30 @@ extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ld
     double *qa = (double *)ws;
     double *qtau = qa + (size_t)k1 * (k2 | 1);
     double *rrow = qtau + k1;
-    {  // one group of 8 (k1 <= 128) or 4 threads per column
-        auto qr = k1 <= 128 ? qr_kernel<8> : qr_kernel<4>;
+    {  // one group of 8 (k1 <= 128) or 4 threads per column; register-resident
+       // columns when they fit 16 registers per thread
+        void (*qr)(const double *, int, int, int64_t, double *, double *, double *) =
+            k1 <= 128 ? qr_kernel<8> : qr_kernel<4>;
+        const char *qv = getenv("SRLU_QR");  // testing knob: smem | reg (default: lookahead)
+        if (k1 <= 128 && k2 <= 128 && qv && !strcmp(qv, "reg")) qr = qr_reg_kernel<16>;
+        else if (k1 * 8 + 32 <= 1024 && !(qv && !strcmp(qv, "smem"))) {
+            qr = nullptr;  // qr_la_kernel<8>
+            smem += sizeof(uint64_t) * (size_t)k1;
+        }
         SRLU_REQUIRE(k1 <= 256, SRLU_ERR_UNSUPPORTED, "qr_pinv: k1 > 256");
-        SRLU_CUDA(cudaFuncSetAttribute(qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        qr<<<1, 1024, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau, rrow);
+        if (qr == nullptr)
+            SRLU_CUDA(cudaFuncSetAttribute(qr_la_kernel<8>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        else
+            SRLU_CUDA(cudaFuncSetAttribute(qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (qr == nullptr) {
+            const char *dv = getenv("SRLU_QR_DEPTH");  // testing knob
+            const int depth = dv ? atoi(dv) : 1;  // measured: 1 < 2 < 3 < 4 (tools/time_qr.py)
+            SRLU_REQUIRE(depth >= 1, SRLU_ERR_ARG, "qr_pinv: SRLU_QR_DEPTH must be >= 1");
+            qr_la_kernel<8><<<1, 1024, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau, rrow, depth);
+        } else {
+            qr<<<1, 1024, smem, s>>>(mT, (int)k1, (int)k2, ldm, qa, qtau, rrow);
+        }
     }
     SRLU_CHECK_LAUNCH("qr_kernel");
     const unsigned tail_grid = (unsigned)ceil_div(k2, 8);
