@@ -1884,6 +1884,33 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
         // ======== phase C: the panel's trailing update (all CTAs) ========
         {
             const int twp = (tw + 15) & ~15;
+            // (entity, column group) per thread: consecutive threads take
+            // consecutive entities of the same columns (coalesced in wt).
+            // Everything that does not depend on the pivot rows — the
+            // frozen-pivot check, the entity's multipliers and its first
+            // block of trailing values — is loaded before the pivot-row
+            // rounds below, so those latencies overlap.
+            constexpr int NI = 3;
+            const int ngrp = neT > 0 ? max(1, (int)blockDim.x / neT) : 1;
+            const int el = neT > 0 ? tid % neT : 0, grp = neT > 0 ? tid / neT : ngrp;
+            const int64_t e = eT0 + el;
+            const bool cact = neT > 0 && grp < ngrp;
+            const int gp_e = cact ? __ldcg(hp.gpos + e) : 0;
+            double l[B];
+            double v[NI][4];
+#pragma unroll
+            for (int ls = 0; ls < B; ++ls)
+                l[ls] = cact && ls < bw ? __ldcg(wt + (int64_t)(J + ls) * ldt + e) : 0.0;
+            {
+                const int cb = 4 * grp;
+#pragma unroll
+                for (int q = 0; q < NI; ++q)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int c = cb + q * 4 * ngrp + i;
+                        v[q][i] = cact && c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + e) : 0.0;
+                    }
+            }
             for (int t = tid; t < bw * B; t += blockDim.x) PR[t] = __ldcg(hp.gPR + t);
             if (tid < bw) s_pw[tid] = __ldcg(hp.gpw + tid);
             __syncthreads();
@@ -1910,29 +1937,21 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
                 }
             }
             __syncthreads();
-            // (entity, column group) per thread: consecutive threads take
-            // consecutive entities of the same columns (coalesced in wt)
-            if (neT > 0) {
-                const int ngrp = max(1, (int)blockDim.x / neT);
-                const int el = tid % neT, grp = tid / neT;
-                const int64_t e = eT0 + el;
-                if (grp < ngrp && __ldcg(hp.gpos + e) >= x0) {  // pivots are frozen
-                    double l[B];
-#pragma unroll
-                    for (int ls = 0; ls < B; ++ls)
-                        l[ls] = ls < bw ? __ldcg(wt + (int64_t)(J + ls) * ldt + e) : 0.0;
+            {
+                if (cact && gp_e >= x0) {  // pivots are frozen
                     // columns 4*grp + {0..3} + 4*ngrp*it, three such groups
-                    // (twelve independent loads) in flight per thread
-                    constexpr int NI = 3;
+                    // (twelve independent loads) in flight per thread; the
+                    // first block was prefetched above
                     for (int cb = 4 * grp; cb < tw; cb += NI * 4 * ngrp) {
-                        double v[NI][4];
+                        if (cb != 4 * grp) {
 #pragma unroll
-                        for (int q = 0; q < NI; ++q)
+                            for (int q = 0; q < NI; ++q)
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const int c = cb + q * 4 * ngrp + i;
-                                v[q][i] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + e) : 0.0;
-                            }
+                                for (int i = 0; i < 4; ++i) {
+                                    const int c = cb + q * 4 * ngrp + i;
+                                    v[q][i] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + e) : 0.0;
+                                }
+                        }
 #pragma unroll
                         for (int q = 0; q < NI; ++q) {
                             const int c0 = cb + q * 4 * ngrp;
