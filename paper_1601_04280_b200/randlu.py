@@ -256,6 +256,7 @@ def _pipeline(a: Matrix, params: RandLuParams, keep: bool, gaussian: bool = Fals
 
 
 _SIDE_STREAMS = {}
+_SMALL_A_BYTES = 256 << 20
 
 
 _EVENTS = threading.local()
@@ -315,18 +316,29 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
         flag = torch.empty(1, dtype=torch.int32, device=dev)
         om1 = composite_sketch_right(a, k1, params.l1, kind, params.seed + 2 * attempt, y, flag)
     ev[1].record(main)
-    # Omega2 (draws + plan + member table of L1) on the side stream while K1
-    # runs (independent of everything enqueued so far)
-    with torch.cuda.stream(side):
-        om2 = build_composite(k2, params.l2, m, kind, params.seed + 2 * attempt + 1, dev)
-        om2.sem.plan()
-        mrow_l, msign_l, bptr2 = members(om2, None, 0, m, stream=side)
-        ev_om2 = torch.cuda.Event()
-        ev_om2.record(side)
 
+    def omega2():
+        # Omega2 (draws + plan + member table of L1) on the side stream,
+        # independent of everything enqueued so far
+        with torch.cuda.stream(side):
+            om = build_composite(k2, params.l2, m, kind, params.seed + 2 * attempt + 1, dev)
+            om.sem.plan()
+            mem = members(om, None, 0, m, stream=side)
+            e = torch.cuda.Event()
+            e.record(side)
+        return om, mem, e
+
+    # A stream shorter than the host side of the Omega2 build (~0.15 ms):
+    # enqueue K2 first so that it does not wait for that host work; longer
+    # streams: Omega2 first, its device work overlapping K1
+    small = not a.is_sparse and a.raw.numel() * a.raw.element_size() < _SMALL_A_BYTES
+    if not small:
+        om2, (mrow_l, msign_l, bptr2), ev_om2 = omega2()
     y_keep = y.clone() if keep else None
     perm, l1, _ = lu_row_pivot_dev(y)
     ev[2].record(main)
+    if small:
+        om2, (mrow_l, msign_l, bptr2), ev_om2 = omega2()
 
     # stage 2: Omega2 L1, then (K4 on the side stream) || Omega2 (P A)
     main.wait_event(ev_om2)
