@@ -163,14 +163,16 @@ __device__ __forceinline__ double wht_pick(const double *row, int bsize, int o, 
 // blocks (nb = pad/bsize <= 16 of them, swizzled) were transformed in
 // place: the remaining stages h = bsize, 2*bsize, ... combine the blocks at
 // offset q % bsize in the reference's order (output-pruned, wht_pick).
-__device__ __forceinline__ double fwht_combine_blocks(const double *row, int bsize, int nb, int q) {
+// Blocks b >= nzb are not stored (all zero).
+__device__ __forceinline__ double fwht_combine_blocks(const double *row, int bsize, int nb, int q,
+                                                      int nzb = 16) {
     const int o = fwht_sw(q & (bsize - 1)), B = q / bsize;
     switch (nb) {
         case 1: return row[o];
-        case 2: return wht_pick<2>(row, bsize, o, B);
-        case 4: return wht_pick<4>(row, bsize, o, B);
-        case 8: return wht_pick<8>(row, bsize, o, B);
-        default: return wht_pick<16>(row, bsize, o, B);
+        case 2: return wht_pick<2>(row, bsize, o, B, nzb);
+        case 4: return wht_pick<4>(row, bsize, o, B, nzb);
+        case 8: return wht_pick<8>(row, bsize, o, B, nzb);
+        default: return wht_pick<16>(row, bsize, o, B, nzb);
     }
 }
 

@@ -135,23 +135,41 @@ __global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ 
                                                      int64_t ldo) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *xs = reinterpret_cast<double *>(smem_raw);
-    const int ldx = pad + 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t c0 = (int64_t)blockIdx.x * CB;
-    const int nc = (int)((n - c0) < CB ? (n - c0) : CB);
-    for (int w = threadIdx.x; w < pad * CB; w += blockDim.x) {
-        const int t = w / CB, c = w % CB;
-        double v = 0.0;
-        if (t < l && c < nc) {
-            v = S[(int64_t)t * n + c0 + c];
-            if (phase[t] < 0.0) v = -v;
-        }
-        xs[c * ldx + fwht_sw(t)] = v;
-    }
-    __syncthreads();
+    // only the bsize-blocks that hold buckets are stored (the rest stay zero
+    // through the in-block stages; the pruned combine treats them as zeros)
     const int bsize = pad < 1024 ? pad : 1024;
     const int nb = pad / bsize;  // <= 8 for pad2 <= 8192
     const int nzb = (l + bsize - 1) / bsize;
+    const int xlen = nzb * bsize;
+    const int ldx = xlen + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * CB;
+    const int nc = (int)((n - c0) < CB ? (n - c0) : CB);
+    // U loads in flight per thread (the tile is read once from HBM; one at
+    // a time left each CTA waiting ~pad*CB/blockDim round trips)
+    constexpr int U = 8;
+    const int total = xlen * CB;
+    for (int w0 = threadIdx.x; w0 < total; w0 += U * blockDim.x) {
+        double v[U];
+        bool neg[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int w = w0 + u * blockDim.x;
+            const int t = w / CB, c = w % CB;
+            const bool ld = w < total && t < l && c < nc;
+            v[u] = ld ? S[(int64_t)t * n + c0 + c] : 0.0;
+            neg[u] = ld && phase[t] < 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int w = w0 + u * blockDim.x;
+            if (w < total) {
+                const int t = w / CB, c = w % CB;
+                xs[c * ldx + fwht_sw(t)] = neg[u] ? -v[u] : v[u];
+            }
+        }
+    }
+    __syncthreads();
     for (int item = warp; item < nc * nzb; item += nw) {
         const int c = item / nzb, b = item % nzb;
         fwht_block_warp_dyn(xs + c * ldx + b * bsize, bsize, lane);
@@ -159,7 +177,8 @@ __global__ void __launch_bounds__(512) k3b_v2_kernel(const double *__restrict__ 
     __syncthreads();
     for (int w = threadIdx.x; w < nc * k; w += blockDim.x) {
         const int c = w / k, kk = w % k;
-        out[(c0 + c) * ldo + kk] = __dmul_rn(fwht_combine_blocks(xs + c * ldx, bsize, nb, idx[kk]), mult);
+        out[(c0 + c) * ldo + kk] =
+            __dmul_rn(fwht_combine_blocks(xs + c * ldx, bsize, nb, idx[kk], nzb), mult);
     }
 }
 
@@ -305,9 +324,11 @@ int launch_k3b(const double *S, int64_t n, int64_t l2, int64_t pad2, const doubl
     }
     if (pad2 >= 32 && pad2 <= 8192) {
         int CB = (int)(16384 / pad2);  // ~128 KB of smem
+        if (const char *e = getenv("SRLU_K3B_V2CB")) CB = atoi(e);  // testing knob
         if (CB < 1) CB = 1;
         if (CB > 64) CB = 64;
-        size_t smem = (size_t)(pad2 + 1) * CB * 8;
+        const int64_t bs2 = pad2 < 1024 ? pad2 : 1024;
+        size_t smem = (size_t)(ceil_div(l2, bs2) * bs2 + 1) * CB * 8;
         SRLU_CUDA(cudaFuncSetAttribute(k3b_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
         k3b_v2_kernel<<<(unsigned)ceil_div(n, CB), 512, smem, stream>>>(

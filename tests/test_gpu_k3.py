@@ -21,7 +21,8 @@ def P():
 
 @pytest.mark.parametrize("m,n,l,k", [(300, 18, 104, 26), (300, 240, 104, 26),
                                      (2000, 64, 104, 26), (600, 18, 472, 118),
-                                     (500, 35, 104, 26), (3000, 97, 900, 200)])
+                                     (500, 35, 104, 26), (3000, 97, 900, 200),
+                                     (3000, 37, 2232, 558)])  # config-5 pad2 4096: K3b v2, 4 columns per CTA
 @pytest.mark.parametrize("v2", [False, True])
 def test_sketch_left_bit_exact(P, monkeypatch, m, n, l, k, v2):
     from oracle import draws as D
