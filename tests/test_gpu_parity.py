@@ -368,3 +368,21 @@ def test_csr_crowded_buckets_bit_exact(P, dt):
     np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
     np.testing.assert_array_equal(res.P.indices, ref["P"])
     np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
+
+
+@pytest.mark.parametrize("n,dt", [(301, np.float32), (299, np.float64)])
+def test_stage1_unaligned_rows_fused_call(P, n, dt):
+    """Rows whose pitch is not a multiple of 16 bytes take the unscheduled K1
+    inside the one-call stage 1 (srlu_composite_sketch_right_dense without a
+    schedule): Y and P still bit-exact against the oracle."""
+    import torch
+    from oracle import randlu as O
+    rng = np.random.default_rng(n)
+    a = (rng.standard_normal((400, 12)) @ rng.standard_normal((12, n))
+         + 1e-3 * rng.standard_normal((400, n))).astype(dt)
+    prm = dict(r=12, k1=20, l1=80, k2=28, l2=112, seed=3)
+    res = P.sparse_randomized_lu(P.Matrix.from_device(torch.from_numpy(a).cuda()),
+                                 P.RandLuParams(**prm), keep=True)
+    ref = O.sparse_randomized_lu(a.astype(np.float64), prm, keep=True)
+    np.testing.assert_array_equal(res.extras["Y"].cpu().numpy(), ref["Y"])
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
