@@ -1919,24 +1919,41 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
                 Ach[ls * AW + c] = c < tw ? __ldcg(wt + (int64_t)(x0 + c) * ldt + s_pw[ls]) : 0.0;
             }
             __syncthreads();
+            LU_T(5);
+            // the panel's pivot rows on the trailing columns: the small
+            // triangular recurrence in registers, fully unrolled so that the
+            // independent chains of different ls overlap (each chain keeps
+            // the reference's l2 order)
             for (int c = tid; c < tw; c += blockDim.x) {
-                for (int ls = 0; ls < bw; ++ls) {
-                    double v = Ach[ls * AW + c];
-                    const double *pr = PR + ls * B;
-                    if (MODE == MODE_ROW) {
+                double a[B];
+#pragma unroll
+                for (int ls = 0; ls < B; ++ls) a[ls] = ls < bw ? Ach[ls * AW + c] : 0.0;
+#pragma unroll
+                for (int ls = 0; ls < B; ++ls) {
+                    if (ls < bw) {
+                        double v = a[ls];
+                        const double *pr = PR + ls * B;
+#pragma unroll
                         for (int l2 = 0; l2 < ls; ++l2)
-                            v = __dsub_rn(v, __dmul_rn(pr[l2], Ach[l2 * AW + c]));
-                    } else {
-                        for (int l2 = 0; l2 < ls; ++l2)
-                            v = __dsub_rn(v, __dmul_rn(Ach[l2 * AW + c], pr[l2]));
-                        const double pv = pr[ls];
-                        v = fabs(pv) > thresh ? v / pv : 0.0;
+                            v = MODE == MODE_ROW ? __dsub_rn(v, __dmul_rn(pr[l2], a[l2]))
+                                                 : __dsub_rn(v, __dmul_rn(a[l2], pr[l2]));
+                        if (MODE != MODE_ROW) {
+                            const double pv = pr[ls];
+                            v = fabs(pv) > thresh ? v / pv : 0.0;
+                        }
+                        a[ls] = v;
                     }
-                    Ach[ls * AW + c] = v;
-                    if (bid == 0) p.piv[(int64_t)(J + ls) * k + x0 + c] = v;
+                }
+#pragma unroll
+                for (int ls = 0; ls < B; ++ls) {
+                    if (ls < bw) {
+                        Ach[ls * AW + c] = a[ls];
+                        if (bid == 0) p.piv[(int64_t)(J + ls) * k + x0 + c] = a[ls];
+                    }
                 }
             }
             __syncthreads();
+            LU_T(7);
             {
                 if (cact && gp_e >= x0) {  // pivots are frozen
                     // columns 4*grp + {0..3} + 4*ngrp*it, three such groups
