@@ -54,6 +54,7 @@ namespace srlu {
 enum { MODE_ROW = 0, MODE_COL = 1 };
 
 constexpr int kLuThreads = 512;
+static_assert(kLuThreads >= 8 * 64, "grid LU: the blocked recurrence uses 8 groups of kLuXC threads");
 constexpr int kLuRPW = 4;  // trailing update: rows per warp pass
 #ifndef SRLU_LU_PFD
 #define SRLU_LU_PFD 1  // trailing update: passes of loads in flight (2 measured: no gain)
@@ -450,25 +451,59 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 Ach[ls * kLuXC + c] = __ldcg(p.w + (int64_t)pw_ent[ls] * p.ld + x0 + c);
             }
             __syncthreads();
-            for (int c = tid; c < xc; c += blockDim.x) {
-                const int x = x0 + c;
-                for (int ls = 0; ls < bw; ++ls) {
-                    double v = Ach[ls * kLuXC + c];
-                    const double *pr = PR + ls * b;
-                    if (MODE == MODE_ROW) {
-                        for (int l2 = 0; l2 < ls; ++l2)
-                            v = __dsub_rn(v, __dmul_rn(pr[l2], Ach[l2 * kLuXC + c]));
-                    } else {
-                        for (int l2 = 0; l2 < ls; ++l2)
-                            v = __dsub_rn(v, __dmul_rn(Ach[l2 * kLuXC + c], pr[l2]));
-                        const double pv = pr[ls];
-                        v = fabs(pv) > thresh ? v / pv : 0.0;
+            // The pivot rows' values on these columns: the triangular
+            // recurrence v(ls) = A(ls) - sum_{l2 < ls} PR(ls, l2) v(l2), each
+            // chain in the reference's l2 order, blocked by 8 rows: the terms
+            // l2 < s of the 8 chains of block [s, s+8) run in parallel (one
+            // thread group per chain, 64 columns each), the in-block terms in
+            // registers by one thread per column.  Wide panels (config 5:
+            // ~50 rows) no longer run 50^2/2 dependent steps per column.
+            {
+                constexpr int KB = 8;
+                const int c = tid % kLuXC, g = tid / kLuXC;
+                for (int s0 = 0; s0 < bw; s0 += KB) {
+                    const int ls = s0 + g;
+                    if (s0 > 0 && g < KB && ls < bw && c < xc) {
+                        double v = Ach[ls * kLuXC + c];
+                        const double *pr = PR + ls * b;
+                        for (int l2 = 0; l2 < s0; ++l2)
+                            v = MODE == MODE_ROW ? __dsub_rn(v, __dmul_rn(pr[l2], Ach[l2 * kLuXC + c]))
+                                                 : __dsub_rn(v, __dmul_rn(Ach[l2 * kLuXC + c], pr[l2]));
+                        Ach[ls * kLuXC + c] = v;
                     }
-                    Ach[ls * kLuXC + c] = v;
-                    if (blockIdx.x == 0) p.piv[(int64_t)(J + ls) * k + x] = v;
+                    __syncthreads();
+                    if (g == 0 && c < xc) {
+                        const int nb = min(KB, bw - s0);
+                        double a[KB];
+#pragma unroll
+                        for (int i = 0; i < KB; ++i) a[i] = i < nb ? Ach[(s0 + i) * kLuXC + c] : 0.0;
+#pragma unroll
+                        for (int i = 0; i < KB; ++i) {
+                            if (i < nb) {
+                                double v = a[i];
+                                const double *pr = PR + (s0 + i) * b + s0;
+#pragma unroll
+                                for (int j = 0; j < i; ++j)
+                                    v = MODE == MODE_ROW ? __dsub_rn(v, __dmul_rn(pr[j], a[j]))
+                                                         : __dsub_rn(v, __dmul_rn(a[j], pr[j]));
+                                if (MODE != MODE_ROW) {
+                                    const double pv = pr[i];
+                                    v = fabs(pv) > thresh ? v / pv : 0.0;
+                                }
+                                a[i] = v;
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < KB; ++i) {
+                            if (i < nb) {
+                                Ach[(s0 + i) * kLuXC + c] = a[i];
+                                if (blockIdx.x == 0) p.piv[(int64_t)(J + s0 + i) * k + x0 + c] = a[i];
+                            }
+                        }
+                    }
+                    __syncthreads();
                 }
             }
-            __syncthreads();
             // rows by warp (RPW per pass), columns by lane (up to two per
             // lane): coalesced, division-free; the next pass's loads are
             // issued before this pass's arithmetic (software pipeline)
