@@ -1599,7 +1599,14 @@ struct LuHybridParams {
     double *gPR;  // [B][B] the panel's pivot rows (panel part)
     int *gpw;     // [B] the panel's pivot entities
     double *gpart;  // [G] partial sums of squares
+    unsigned *cnt;  // CTAs done with the next panel's columns (zeroed per launch)
 };
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 template <int MODE, int B, int RPT>
 __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams hp) {
@@ -1756,6 +1763,7 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
     __syncthreads();
     const double thresh = s_thresh;
     LU_T0();
+    int npan = 0;
 
     for (int J = 0; J < k; J += b) {
         const int bw = min(b, k - J);
@@ -1989,13 +1997,23 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
             }
             __syncthreads();
             LU_T(7);
-            {
+            // columns 4*grp + {0..3} + 4*ngrp*it, three such groups (twelve
+            // independent loads) in flight per thread.  Pass 1 = the first
+            // block (prefetched above; it holds every column of the next
+            // panel), then a signal to cluster 0, then pass 2 = the rest.
+            for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 1) {
+                    __syncthreads();
+                    if (tid == 0) {
+                        __threadfence();
+                        atomicAdd(hp.cnt, 1u);
+                    }
+                }
                 if (cact && gp_e >= x0) {  // pivots are frozen
-                    // columns 4*grp + {0..3} + 4*ngrp*it, three such groups
-                    // (twelve independent loads) in flight per thread; the
-                    // first block was prefetched above
-                    for (int cb = 4 * grp; cb < tw; cb += NI * 4 * ngrp) {
-                        if (cb != 4 * grp) {
+                    const int cb0 = 4 * grp + (pass ? NI * 4 * ngrp : 0);
+                    const int cb1 = pass ? tw : min(tw, 4 * grp + 1);
+                    for (int cb = cb0; cb < cb1; cb += NI * 4 * ngrp) {
+                        if (pass) {
 #pragma unroll
                             for (int q = 0; q < NI; ++q)
 #pragma unroll
@@ -2028,7 +2046,16 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
             }
         }
         LU_T(2);
-        grid.sync();
+        // cluster 0 waits only until every CTA has updated the next panel's
+        // columns (pass 1); the rest of the trailing update overlaps the
+        // next panel's pivot steps.  The next panel's grid barrier orders
+        // everyone's pass 2 before its own phase C.
+        ++npan;
+        if (panel_cta) {
+            if (tid == 0)
+                while (ld_acquire_gpu(hp.cnt) < (unsigned)(npan * G)) __nanosleep(32);
+            __syncthreads();
+        }
         LU_T(3);
     }
     LU_TDUMP();
@@ -2205,6 +2232,8 @@ static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool
     hp.gpart = (double *)extra;
     extra += 256 * sizeof(double);
     hp.gpw = (int *)extra;
+    hp.cnt = (unsigned *)(extra + 128);  // gpw holds <= 16 ints
+    SRLU_CUDA(cudaMemsetAsync(hp.cnt, 0, sizeof(unsigned), stream));
     (void)G;
     SRLU_CUDA(cudaLaunchKernelEx(&cfg, kern, hp));
     *launched = true;
