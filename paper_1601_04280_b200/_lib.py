@@ -116,8 +116,8 @@ def lib():
 class _LaunchCounter:
     """Number of libsrlu kernels enqueued (bench.py's ``gpu_launches``)."""
 
-    PER_CALL = {"build_sem": 3, "sem_plan": 4, "build_composite": 7, "build_composite_k1": 9, "composite_sketch_right_dense": 10, "composite_sketch_right_dense_nosched": 8, "sketch_right_dense": 1, "sketch_right_csr": 1,
-                "k1_schedule": 2, "sketch_right_dense_sched": 1,
+    PER_CALL = {"build_sem": 3, "sem_plan": 4, "build_composite": 7, "build_composite_k1": 8, "build_composite_k1_g": 9, "composite_sketch_right_dense": 9, "composite_sketch_right_dense_g": 10, "composite_sketch_right_dense_nosched": 8, "sketch_right_dense": 1, "sketch_right_csr": 1,
+                "k1_schedule": 2, "k1_schedule_1": 1, "sketch_right_dense_sched": 1,
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 6,
                 "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1,

@@ -96,12 +96,22 @@ class SparseEmbedding:
             buf = torch.empty(nbytes, dtype=torch.uint8, device=srt.device)
             _lib.check(L.srlu_k1_schedule(_lib.ptr(srt), _lib.ptr(bptr), self.in_dim, self.out_dim,
                                           pad, dtype_code, _lib.ptr(buf), nbytes,
-                                          _lib.stream_handle(stream)), "k1_schedule")
+                                          _lib.stream_handle(stream)),
+                       "k1_schedule" if _k1_grouped(L, self.in_dim, self.out_dim, pad, dtype_code)
+                       else "k1_schedule_1")
         self._sched.append((key, buf))
         return buf
 
     def row_counts(self):
         return torch.bincount(self.row_of.long(), minlength=self.out_dim)
+
+
+def _k1_grouped(L, n, l, pad, dtype_code) -> bool:
+    """Whether the K1 schedule for this shape runs the group-sort kernel
+    (several bucket slots per lane)."""
+    info = (ctypes.c_int64 * 8)()
+    L.srlu_k1_config(n, l, pad, dtype_code, info)
+    return info[1] >= 2
 
 
 def build_sem(k, n, seed, device=None) -> SparseEmbedding:
@@ -249,6 +259,9 @@ def _composite_layout(L, k, l, n, k1_dtype):
             sched_bytes = L.srlu_k1_schedule_bytes(n, l, _next_pow2(l), k1_dtype)
         off["sched"] = (off["ws"] + ws_bytes + 255) // 256 * 256
         total = off["sched"] + max(sched_bytes, 0)
+        # the schedule builder's extra group-sort kernel runs only for
+        # multi-slot lanes (srlu_k1_config info[1] = buckets per lane >= 2)
+        off["grouped"] = bool(sched_bytes) and _k1_grouped(L, n, l, _next_pow2(l), k1_dtype)
         lay = (off, ws_bytes, sched_bytes, total, L.srlu_build_composite_staging(k, l))
         _LAYOUTS[key] = lay
     return lay
@@ -306,7 +319,8 @@ def _composite(k, l, n, kind, seed, device, stream, k1_dtype, right):
             ctypes.addressof(padc), staging.data_ptr(), staging.numel(), P_(base + off["ws"]),
             ws_bytes, -1 if k1_dtype is None else k1_dtype,
             P_(base + off["sched"]) if sched_bytes else None, sched_bytes, sh),
-            "build_composite_k1" if sched_bytes else "build_composite")
+            ("build_composite_k1_g" if off["grouped"] else "build_composite_k1") if sched_bytes
+            else "build_composite")
     else:
         t, dcode, y, nonfinite = right
         m = t.shape[0]
@@ -318,7 +332,8 @@ def _composite(k, l, n, kind, seed, device, stream, k1_dtype, right):
             P_(t.data_ptr()), dcode, m, t.stride(0), math.sqrt(pad / k) / math.sqrt(pad),
             P_(y.data_ptr()),
             y.stride(0), P_(nonfinite.data_ptr()), sh),
-            "composite_sketch_right_dense" if sched_bytes else "composite_sketch_right_dense_nosched")
+            ("composite_sketch_right_dense_g" if off["grouped"] else "composite_sketch_right_dense")
+            if sched_bytes else "composite_sketch_right_dense_nosched")
     _STAGING.put(staging, stream if stream is not None else torch.cuda.current_stream(dev))
     assert padc.value == pad
     isz = {torch.float64: 8, torch.int32: 4}
