@@ -256,10 +256,34 @@ int srlu_qr_rank(const void *ws, int64_t k1, int64_t k2, double *stats, srlu_str
 int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, const double *RT, int64_t ldt,
                        double *stats, srlu_stream_t stream);
 
-/* C (M x N) = A (M x K) · B (K x N), row-major fp64 (matrix.py:219-230 matmul
- * for randlu.py:267 and :272) */
+/* ---- FP64 tensor-core GEMMs (DMMA) and the approximation error (K7) ---- */
+
+/* C (M x N) = A (M x K) · B (K x N), row-major fp64 on the FP64 tensor cores
+ * (matrix.py:219-230 matmul for randlu.py:267 core = pinv·(Omega2 P A) and
+ * randlu.py:272 L = L1·L~).  srlu_dgemm_ex flags: SRLU_GEMM_B_LOWER — B is
+ * lower triangular (B[j][c] == 0 for j < c, like L~), the zero blocks are
+ * skipped. */
+#define SRLU_GEMM_B_LOWER 1
 int srlu_dgemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                int64_t ldc, int64_t M, int64_t N, int64_t K, srlu_stream_t stream);
+int srlu_dgemm_ex(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                  int64_t ldc, int64_t M, int64_t N, int64_t K, int flags,
+                  srlu_stream_t stream);
+
+/* approximation_error (randlu.py:279-302): *sq (device) = ||L U - P A Q||_F^2
+ * for L (m x k row-major, positions), U given as UT (n x k row-major, U^T),
+ * perm[m] / q[n] the row / column permutations, A dense (m x n, lda) or
+ * CSR (indptr int64[m+1], indices int32 ascending per row, values).  Fixed
+ * summation order: deterministic.  Workspace: srlu_lu_error_workspace. */
+size_t srlu_lu_error_workspace(int64_t m, int64_t n, int64_t k);
+int srlu_lu_error_dense(const double *L, int64_t ldl, const double *UT, int64_t ldut,
+                        const int64_t *perm, const int64_t *q, const void *a, int dtype,
+                        int64_t m, int64_t n, int64_t lda, int64_t k, double *sq, void *ws,
+                        size_t ws_bytes, srlu_stream_t stream);
+int srlu_lu_error_csr(const double *L, int64_t ldl, const double *UT, int64_t ldut,
+                      const int64_t *perm, const int64_t *q, const int64_t *indptr,
+                      const int32_t *indices, const void *vals, int dtype, int64_t m, int64_t n,
+                      int64_t k, double *sq, void *ws, size_t ws_bytes, srlu_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,12 @@ SIGNATURES = {
     "srlu_rank_estimate": (INT, [P, I64, I64, P, I64, P, P]),
     "srlu_qr_rank": (INT, [P, I64, I64, P, P]),
     "srlu_dgemm": (INT, [P, I64, P, I64, P, I64, I64, I64, I64, P]),
+    "srlu_dgemm_ex": (INT, [P, I64, P, I64, P, I64, I64, I64, I64, INT, P]),
+    "srlu_lu_error_workspace": (SZ, [I64, I64, I64]),
+    "srlu_lu_error_dense": (INT, [P, I64, P, I64, P, P, P, INT, I64, I64, I64, I64, P, P, SZ,
+                                  P]),
+    "srlu_lu_error_csr": (INT, [P, I64, P, I64, P, P, P, P, P, INT, I64, I64, I64, P, P, SZ,
+                                P]),
     "srlu_lu_workspace": (SZ, [I64, I64]),
     "srlu_lu_rowpiv": (INT, [P, I64, I64, I64, P, P, I64, P, I64, INT, P, SZ, P]),
     "srlu_lu_colpiv": (INT, [P, I64, I64, I64, P, P, I64, P, I64, INT, P, SZ, P]),
@@ -121,7 +127,7 @@ class _LaunchCounter:
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 6,
                 "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1,
-                "dgemm": 1}
+                "dgemm": 1, "lu_error": 3}
 
     def __init__(self):
         self.total = 0

@@ -13,9 +13,6 @@
 //    within the estimators' slack of 1e10.
 //  * srlu_rank_estimate: the same test on an R in global memory (used when
 //    M does not fit one CTA; the QR then comes from cuSOLVER).
-//  * srlu_dgemm: C = A·B row-major fp64 SIMT-FMA GEMM for the skinny core
-//    and L products (cuBLAS picks a 32x32 DMMA tile that reached <3 TFLOP/s
-//    on the 16384x118x110 shape).
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -530,64 +527,6 @@ __global__ void __launch_bounds__(256, 1) rank_estimate_kernel(const double *__r
     rank_estimate(R, ldr, RT, ldt, k, xv, yv, red, stats);
 }
 
-// ---------------------------------------------------------------------------
-// C (M x N) = A (M x K) . B (K x N), row-major fp64, FMA.
-
-constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
-
-__global__ void __launch_bounds__(256) dgemm_kernel(const double *__restrict__ A, int64_t lda,
-                                                    const double *__restrict__ B, int64_t ldb,
-                                                    double *__restrict__ C, int64_t ldc,
-                                                    int64_t M, int N, int K) {
-    __shared__ double As[kGemmBK][kGemmBM + 2];
-    __shared__ double Bs[kGemmBK][kGemmBN + 2];
-    const int tid = threadIdx.x;
-    const int tx = tid % 16, ty = tid / 16;
-    const int64_t m0 = (int64_t)blockIdx.x * kGemmBM;
-    const int n0 = blockIdx.y * kGemmBN;
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    for (int k0 = 0; k0 < K; k0 += kGemmBK) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int e = tid + i * 256;  // 0..1023
-            const int am = e / kGemmBK, ak = e % kGemmBK;
-            const int64_t gm = m0 + am;
-            const int gk = k0 + ak;
-            As[ak][am] = (gm < M && gk < K) ? A[gm * lda + gk] : 0.0;
-            const int bk = e / kGemmBN, bn = e % kGemmBN;
-            const int gk2 = k0 + bk, gn = n0 + bn;
-            Bs[bk][bn] = (gk2 < K && gn < N) ? B[(int64_t)gk2 * ldb + gn] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < kGemmBK; ++kk) {
-            double a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t gm = m0 + ty * 4 + i;
-        if (gm >= M) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gn = n0 + tx + 16 * j;
-            if (gn < N) C[gm * ldc + gn] = acc[i][j];
-        }
-    }
-}
 
 static size_t qr_pinv_smem(int64_t k1, int64_t k2) {
     const int64_t ld = k2 | 1;
@@ -967,16 +906,6 @@ extern "C" int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, const
     return SRLU_OK;
 }
 
-extern "C" int srlu_dgemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
-                          int64_t ldc, int64_t M, int64_t N, int64_t K, srlu_stream_t stream) {
-    SRLU_REQUIRE(M >= 0 && N >= 0 && K >= 0 && N < (1 << 30) && K < (1 << 30), SRLU_ERR_ARG,
-                 "dgemm: bad sizes");
-    if (M == 0 || N == 0) return SRLU_OK;
-    dim3 grid((unsigned)ceil_div(M, kGemmBM), (unsigned)ceil_div(N, kGemmBN));
-    dgemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, C, ldc, M, (int)N, (int)K);
-    SRLU_CHECK_LAUNCH("dgemm_kernel");
-    return SRLU_OK;
-}
 
 extern "C" int srlu_qr_rank(const void *ws, int64_t k1, int64_t k2, double *stats,
                             srlu_stream_t stream) {

@@ -97,7 +97,7 @@ class CudaOps:
         pinv_t, stats = pinv_dev(red_lT)
         core_t = dgemm(red_aT, pinv_t)
         q, lt, ut = lu_col_pivot_dev(core_t)
-        l_final = dgemm(l1, lt)
+        l_final = dgemm(l1, lt, b_lower=True)
         return q, l_final, ut, stats
 
 

@@ -3,8 +3,8 @@
 ``lu_row_pivot`` / ``lu_col_pivot`` run the persistent CUDA kernel K2/K5
 (bit-exact replays of factor.py:49-77 / :80-109).  ``left_pseudo_inverse``
 keeps the reference's Householder-QR formulation and sigma-ratio rank test
-(factor.py:112-130); in this round it runs on cuSOLVER through torch.linalg
-(a ≤ 558 x 550 problem, <1% of the step) — see DESIGN.md §5.
+(factor.py:112-130) in libsrlu kernels; ``dgemm`` is libsrlu's FP64
+tensor-core (DMMA) GEMM.
 """
 
 from __future__ import annotations
@@ -149,18 +149,12 @@ def pinv_dev(m_t: torch.Tensor, stream=None, rank_event=False):
     return pinv_t, stats
 
 
-def dgemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None):
-    """out = a @ b (row-major fp64).  These are plain GEMMs (randlu.py:267,
-    :272): cuBLAS DGEMM (measured 1.3-2x faster than libsrlu's SIMT FMA
-    GEMM on these shapes); libsrlu's srlu_dgemm remains available via
-    ``dgemm_srlu``."""
-    if out is None:
-        return torch.mm(a, b)
-    return torch.mm(a, b, out=out)
-
-
-def dgemm_srlu(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None):
-    """out = a @ b (row-major fp64) with libsrlu's FMA GEMM."""
+def dgemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None,
+          b_lower: bool = False):
+    """out = a @ b (row-major fp64) on the FP64 tensor cores (libsrlu
+    srlu_dgemm_ex, DMMA): core = pinv . (Omega2 P A) (randlu.py:267) and
+    L = L1 . L~ (randlu.py:272).  ``b_lower``: b is lower triangular (L~);
+    its zero blocks are skipped."""
     L = _lib.lib()
     a = a if a.stride(1) == 1 else a.contiguous()
     b = b if b.stride(1) == 1 else b.contiguous()
@@ -168,10 +162,13 @@ def dgemm_srlu(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None
     K2, N = b.shape
     if K != K2:
         raise ShapeError(f"inner dimensions differ: {tuple(a.shape)} x {tuple(b.shape)}")
+    if a.dtype != torch.float64 or b.dtype != torch.float64:
+        raise ShapeError("dgemm needs float64 operands")
     if out is None:
         out = torch.empty(M, N, dtype=torch.float64, device=a.device)
-    _lib.check(L.srlu_dgemm(_lib.ptr(a), a.stride(0), _lib.ptr(b), b.stride(0), _lib.ptr(out),
-                            out.stride(0), M, N, K, _lib.stream_handle(stream)), "dgemm")
+    _lib.check(L.srlu_dgemm_ex(_lib.ptr(a), a.stride(0), _lib.ptr(b), b.stride(0), _lib.ptr(out),
+                               out.stride(0), M, N, K, 1 if b_lower else 0,
+                               _lib.stream_handle(stream)), "dgemm")
     return out
 
 

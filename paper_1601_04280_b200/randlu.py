@@ -212,7 +212,7 @@ def _attempt_gaussian(a: Matrix, params: RandLuParams, attempt: int, keep: bool)
     ev[4].record(main)
     core_keep = core_t.clone() if keep else None
     q, lt, ut = lu_col_pivot_dev(core_t)
-    l_final = dgemm(l1, lt)
+    l_final = dgemm(l1, lt, b_lower=True)
     ev[5].record(main)
     ev[5].synchronize()
     check_rank(stats.cpu().numpy())
@@ -375,7 +375,7 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     # one SM left to the side stream's rank test (a cooperative launch would
     # otherwise wait for it)
     q, lt, ut = lu_col_pivot_dev(core_t, reserve_sms=1)
-    l_final = dgemm(l1, lt)
+    l_final = dgemm(l1, lt, b_lower=True)
     ev[5].record(main)
 
     # the one host sync of the attempt: rank test, non-finite flag, P, Q
@@ -411,43 +411,41 @@ def _wrap(t: torch.Tensor) -> Matrix:
     return mm
 
 
-def approximation_error(a, res: RandLuResult, block_cols: int = 4096) -> float:
-    """||L U - P A Q||_F (randlu.py:279-302) on the device, column blocks.
-    Evaluation only (never timed)."""
+def approximation_error(a, res: RandLuResult) -> float:
+    """||L U - P A Q||_F (randlu.py:279-302) on the device: K7
+    (srlu_lu_error_dense / _csr), the L·(U Q^T) tiles on the FP64 tensor
+    cores with P·A subtracted and squared in the epilogue; a fixed summation
+    order (deterministic).  Evaluation only (never timed)."""
     if not isinstance(a, Matrix):
         a = Matrix.from_device(a) if isinstance(a, torch.Tensor) and a.is_cuda else Matrix(a)
     m, n = a.shape
     if res.L.rows != m or res.U.cols != n or res.L.cols != res.U.rows \
             or res.P.size != m or res.Q.size != n:
         raise ShapeError(f"factors {res.L.shape} x {res.U.shape} do not match target {a.shape}")
+    lib = _lib.lib()
     dev = a.device
+    k = res.L.cols
     perm = res.P.device_indices(dev)
     cols = res.Q.device_indices(dev)
     ld = res.L.to_dense().to(torch.float64)
-    ud = res.U.to_dense().to(torch.float64)
-    acc = torch.zeros((), dtype=torch.float64, device=dev)
+    ld = ld if ld.stride(1) == 1 else ld.contiguous()
+    ut = res.U.to_dense().to(torch.float64).t()        # n x k (U^T)
+    ut = ut if ut.stride(1) == 1 else ut.contiguous()
+    ws = _lib.workspace(lib.srlu_lu_error_workspace(m, n, k), dev)
+    sq = torch.empty(1, dtype=torch.float64, device=dev)
+    sh = _lib.stream_handle()
     if a.is_sparse:
         indptr, indices, vals = a.raw
-        rows = torch.repeat_interleave(torch.arange(m, device=dev), indptr.diff())
-        inv_perm = torch.empty_like(perm)
-        inv_perm[perm] = torch.arange(m, device=dev)
-        inv_q = torch.empty_like(cols)
-        inv_q[cols] = torch.arange(n, device=dev)
-        prow = inv_perm[rows]
-        pcol = inv_q[indices.long()]
-        for start in range(0, n, block_cols):
-            stop = min(n, start + block_cols)
-            blk = ld @ ud[:, start:stop]
-            sel = (pcol >= start) & (pcol < stop)
-            blk.index_put_((prow[sel], pcol[sel] - start), -vals[sel].to(torch.float64),
-                           accumulate=True)
-            acc += (blk * blk).sum()
+        _lib.check(lib.srlu_lu_error_csr(_lib.ptr(ld), ld.stride(0), _lib.ptr(ut), ut.stride(0),
+                                         _lib.ptr(perm), _lib.ptr(cols), _lib.ptr(indptr),
+                                         _lib.ptr(indices), _lib.ptr(vals),
+                                         _lib.dtype_code(vals.dtype), m, n, k, _lib.ptr(sq),
+                                         _lib.ptr(ws), ws.numel(), sh), "lu_error")
     else:
         t = a.raw
-        for start in range(0, n, block_cols):
-            stop = min(n, start + block_cols)
-            blk = ld @ ud[:, start:stop]
-            ref = t.index_select(1, cols[start:stop]).index_select(0, perm).to(torch.float64)
-            blk -= ref
-            acc += (blk * blk).sum()
-    return math.sqrt(float(acc))
+        _lib.check(lib.srlu_lu_error_dense(_lib.ptr(ld), ld.stride(0), _lib.ptr(ut), ut.stride(0),
+                                           _lib.ptr(perm), _lib.ptr(cols), _lib.ptr(t),
+                                           _lib.dtype_code(t.dtype), m, n, t.stride(0), k,
+                                           _lib.ptr(sq), _lib.ptr(ws), ws.numel(), sh),
+                   "lu_error")
+    return math.sqrt(float(sq.item()))

@@ -1,6 +1,6 @@
 // Microbenchmark: cost of one grid-wide barrier (+ candidate exchange) for a
 // persistent cooperative kernel with one CTA per SM.  Used to pick the
-// barrier used by lu.cu.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+// barrier used by lu.cu.  Build: nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdint>

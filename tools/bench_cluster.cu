@@ -1,6 +1,6 @@
 // Cluster barrier cost on B200: bare cluster.sync, with a one-warp DSMEM push
 // before it, and with the arrive/wait split (relaxed arrive + wait).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bench_cluster.cu -o tools/bench_cluster
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bench_cluster.cu -o tools/bin/bench_cluster
 #include <cooperative_groups.h>
 #include <cstdio>
 namespace cg = cooperative_groups;

@@ -1,7 +1,7 @@
 // FP64 vector-pipe throughput on this GPU: DADD, DMUL and DFMA chains with 8
 // independent accumulators per thread, all SMs.  Prints G ops/s and
 // warp-instructions per clock per SM (at the measured SM clock).
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/bench_fp64.cu -o tools/bench_fp64
+// Build: nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3 tools/bench_fp64.cu -o tools/bin/bench_fp64
 #include <cstdio>
 #include <cuda_runtime.h>
 

@@ -2,7 +2,7 @@
 // does it per pivot step: every CTA pushes NP 16-byte items to every CTA
 // with st.async (complete_tx on the receiver's mbarrier), then waits on its
 // own mbarrier.  Three slots, re-armed after each wait.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bench_xchg.cu -o tools/bench_xchg
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/bench_xchg.cu -o tools/bin/bench_xchg
 #include <cooperative_groups.h>
 #include <cstdio>
 namespace cg = cooperative_groups;

@@ -1,7 +1,7 @@
 // Exhaustive-style check: q = fma(fma(-b, RN(a*y), a), y, RN(a*y)) with
 // y = __drcp_rn(b) equals a / b bit for bit, over random and adversarial
 // (a, b) in the range the LU uses (|a| <= |b|, finite, normal).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false tools/check_div.cu -o tools/check_div
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false tools/check_div.cu -o tools/bin/check_div
 #include <cstdio>
 #include <cstdint>
 

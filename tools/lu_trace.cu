@@ -1,7 +1,7 @@
 // Phase timing of the LU kernels (rank 0, thread 0 clock64 sums).
 // Usage: tools/lu_trace m k [col]
-// Build: nvcc -DSRLU_LU_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false \
-//   -std=c++17 tools/lu_trace.cu paper_1601_04280_b200/csrc/abi.cu -o tools/lu_trace
+// Build: nvcc -cudart shared -DSRLU_LU_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false \
+//   -std=c++17 tools/lu_trace.cu paper_1601_04280_b200/csrc/abi.cu -o tools/bin/lu_trace
 #include <cstdio>
 #include <cstdlib>
 #include <vector>

@@ -1,7 +1,7 @@
 // Can a cooperative launch carry cluster dimensions on this device, how many
 // 16-/8-CTA clusters (1024 threads, ~170 KB smem) are co-resident, and does
 // grid.sync() work across them?
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/probe_coop_cluster.cu -o tools/probe_coop_cluster
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/probe_coop_cluster.cu -o tools/bin/probe_coop_cluster
 #include <cooperative_groups.h>
 #include <cstdio>
 namespace cg = cooperative_groups;

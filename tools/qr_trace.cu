@@ -1,6 +1,6 @@
 // Per-reflector clock64 trace of qr_kernel (critical chain timing).
-// Build: nvcc -DSRLU_QR_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false \
-//   -std=c++17 -I paper_1601_04280_b200/csrc tools/qr_trace.cu paper_1601_04280_b200/csrc/abi.cu -o tools/qr_trace
+// Build: nvcc -cudart shared -DSRLU_QR_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false \
+//   -std=c++17 -I paper_1601_04280_b200/csrc tools/qr_trace.cu paper_1601_04280_b200/csrc/abi.cu -o tools/bin/qr_trace
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
