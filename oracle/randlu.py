@@ -71,6 +71,15 @@ def lib():
         L.oracle_sem_scatter_dense.argtypes = [P, I, I, I, P, P, P, I]
         L.oracle_sem_gather_csc.argtypes = [P, P, P, I, P, P, P, I]
         L.oracle_sem_scatter_csc.argtypes = [P, P, P, I, P, P, P, I]
+        C = ctypes.c_int
+        D = ctypes.c_double
+        L.oracle_lu_blocked.argtypes = [P, I, I, C, D, P, C, I]
+        L.oracle_sketch_right_dense_rows.argtypes = [P, C, I, I, I, P, P, P, I, I, P, I, D, P,
+                                                     I, C]
+        L.oracle_sketch_right_csr_rows.argtypes = [P, P, P, C, I, P, P, P, I, I, P, I, D, P, I,
+                                                   C]
+        L.oracle_sketch_left_dense_cols.argtypes = [P, C, I, I, I, P, P, P, P, I, I, P, I, D, P,
+                                                    I, C]
         _lib = L
     return _lib
 
@@ -221,6 +230,103 @@ def lu_col_pivot(mat):
     lower = np.tril(w[:, :k], -1)
     lower[np.arange(k), np.arange(k)] = 1.0
     return q, np.asfortranarray(lower), np.asfortranarray(np.triu(w))
+
+
+def _lu_blocked(w, mode, thresh, nthreads):
+    w = np.array(w, dtype=np.float64, order="C")          # a copy: factorized in place
+    M, k = w.shape
+    perm = np.empty(M, dtype=np.int64)
+    lib().oracle_lu_blocked(_p(w), M, k, mode, float(thresh), _p(perm), int(nthreads), 32)
+    return w, perm
+
+
+def lu_row_pivot_blocked(y, nthreads=0, thresh=None):
+    """lu_row_pivot (factor.py:49-77) by the blocked multithreaded C
+    restatement (oracle/lu_blocked.c), bit-identical to lu_row_pivot; for
+    the full-size checks.  ``thresh`` defaults to PIVOT_RTOL·||Y||_F computed
+    like the reference (norm of the F-order working copy).  Returns (perm,
+    L m x k C-order, U k x k)."""
+    m, k = y.shape
+    if m < k:
+        raise ValueError(f"need rows >= cols, got {m} x {k}")
+    if thresh is None:
+        thresh = PIVOT_RTOL * np.linalg.norm(np.asfortranarray(y, dtype=np.float64))
+    w, perm = _lu_blocked(y, 0, thresh, nthreads)
+    u = np.triu(w[:k, :k])
+    w[:k, :k] = np.tril(w[:k, :k], -1)
+    w[np.arange(k), np.arange(k)] = 1.0
+    return perm, w, u
+
+
+def lu_col_pivot_blocked(core_t, nthreads=0, thresh=None):
+    """lu_col_pivot (factor.py:80-109) of core = core_t^T by the blocked C
+    restatement, on core_t (n x k: rows of core_t are columns of core).
+    Returns (q, L~ k x k, U k x n)."""
+    n, k = core_t.shape
+    if k > n:
+        raise ValueError(f"need rows <= cols, got {k} x {n}")
+    if thresh is None:
+        thresh = PIVOT_RTOL * np.linalg.norm(np.asfortranarray(np.asarray(core_t).T))
+    w, q = _lu_blocked(core_t, 1, thresh, nthreads)
+    lower = np.triu(w[:k, :k], 1).T.copy()
+    lower[np.arange(k), np.arange(k)] = 1.0
+    return q, lower, np.triu(w.T)
+
+
+def sketch_right_rows(a_rows, om, nthreads=0):
+    """apply_sketch_right (sketch.py:362-368) of a block of rows of A (C
+    order fp32/fp64, or a scipy CSR block with ascending indices), multi-
+    threaded C (oracle/lu_blocked.c); bit-identical to apply_sketch_right
+    on the same rows.  Returns rows x k (C order)."""
+    row_of = np.ascontiguousarray(om["row_of"], dtype=np.int64)
+    sign = np.ascontiguousarray(om["sign"], dtype=np.float64)
+    phase = np.ascontiguousarray(om["phase"], dtype=np.float64)
+    sample = np.ascontiguousarray(om["sample_idx"], dtype=np.int64)
+    k, l, pad = len(sample), om["l"], om["pad"]
+    mult = om["scale"] / math.sqrt(pad)
+    rows = a_rows.shape[0]
+    y = np.empty((rows, k))
+    if issparse(a_rows):
+        indptr = np.ascontiguousarray(a_rows.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(a_rows.indices, dtype=np.int32)
+        vals = np.ascontiguousarray(a_rows.data)
+        dt = 0 if vals.dtype == np.float32 else 1
+        vals = vals if dt == 0 else vals.astype(np.float64)
+        lib().oracle_sketch_right_csr_rows(_p(indptr), _p(indices), _p(vals), dt, rows,
+                                           _p(row_of), _p(sign), _p(phase), l, pad, _p(sample),
+                                           k, mult, _p(y), k, int(nthreads))
+        return y
+    a_rows = np.ascontiguousarray(a_rows)
+    dt = 0 if a_rows.dtype == np.float32 else 1
+    if dt:
+        a_rows = a_rows.astype(np.float64, copy=False)
+    lib().oracle_sketch_right_dense_rows(_p(a_rows), dt, rows, a_rows.shape[1], a_rows.shape[1],
+                                         _p(row_of), _p(sign), _p(phase), l, pad, _p(sample), k,
+                                         mult, _p(y), k, int(nthreads))
+    return y
+
+
+def sketch_left_cols(a_cols, perm, om, nthreads=0):
+    """apply_sketch_left (sketch.py:371-378) of P·A restricted to a block of
+    columns: ``a_cols`` is the m x nb block of A (C order fp32/fp64, rows in
+    A's order), ``perm`` P's indices.  Returns nb x k2 = the block's columns
+    of (Omega2 P A)^T, bit-identical to apply_sketch_left(om, A[perm])."""
+    a_cols = np.ascontiguousarray(a_cols)
+    dt = 0 if a_cols.dtype == np.float32 else 1
+    if dt:
+        a_cols = a_cols.astype(np.float64, copy=False)
+    m, nb = a_cols.shape
+    perm = np.ascontiguousarray(perm, dtype=np.int64)
+    row_of = np.ascontiguousarray(om["row_of"], dtype=np.int64)
+    sign = np.ascontiguousarray(om["sign"], dtype=np.float64)
+    phase = np.ascontiguousarray(om["phase"], dtype=np.float64)
+    sample = np.ascontiguousarray(om["sample_idx"], dtype=np.int64)
+    k, l, pad = len(sample), om["l"], om["pad"]
+    out = np.empty((nb, k))
+    lib().oracle_sketch_left_dense_cols(_p(a_cols), dt, m, nb, nb, _p(perm), _p(row_of),
+                                        _p(sign), _p(phase), l, pad, _p(sample), k,
+                                        om["scale"] / math.sqrt(pad), _p(out), k, int(nthreads))
+    return out
 
 
 def left_pseudo_inverse(mat):
@@ -374,7 +480,7 @@ def forward_error_band(red_l, red_a, l1):
     for i in range(k - 1, -1, -1):
         x[i] = (b[i] - rf[i, i + 1:] @ x[i + 1:]) / rf[i, i]
     core = (x @ np.asarray(red_a, dtype=np.longdouble)).astype(np.float64)
-    q, lt, u = lu_col_pivot(core)
+    q, lt, u = lu_col_pivot_blocked(np.ascontiguousarray(core.T))
     return q, matmul(l1, lt), u
 
 

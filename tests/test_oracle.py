@@ -177,3 +177,64 @@ def test_resample_callback_called_twice():
     calls = []
     O.sparse_randomized_lu(a, prm, on_resample=lambda t, e: calls.append(t))
     assert calls == [0, 1]
+
+
+# --------------------------------------------------------------------------
+# the blocked multithreaded restatement (oracle/lu_blocked.c) used by the
+# full-size checks: pinned to the reference's golden factorizations and to
+# the numpy restatement above, bit for bit
+
+
+def test_blocked_lu_matches_reference_goldens(golden):
+    g = golden("factor.npz")
+    for name, b in cases.factor_cases().items():
+        if b.shape[0] >= b.shape[1]:
+            p, l, u = O.lu_row_pivot_blocked(b, nthreads=3)
+            np.testing.assert_array_equal(p, g[name + "_row_P"], err_msg=name)
+            np.testing.assert_array_equal(l, g[name + "_row_L"], err_msg=name)
+            np.testing.assert_array_equal(u, g[name + "_row_U"], err_msg=name)
+        bt = b.T if b.shape[0] >= b.shape[1] else b
+        q, l, u = O.lu_col_pivot_blocked(np.ascontiguousarray(bt.T), nthreads=3)
+        np.testing.assert_array_equal(q, g[name + "_col_Q"], err_msg=name)
+        np.testing.assert_array_equal(l, g[name + "_col_L"], err_msg=name)
+        np.testing.assert_array_equal(u, g[name + "_col_U"], err_msg=name)
+
+
+@pytest.mark.parametrize("m,k,kind,threads", [
+    (2000, 60, "gauss", 4), (5000, 110, "gauss", 7), (3000, 37, "gauss", 1),
+    (4000, 40, "lowrank", 3), (600, 40, "ties", 5), (12000, 100, "gauss", 8)])
+def test_blocked_lu_matches_numpy_restatement(m, k, kind, threads):
+    rng = np.random.default_rng(m + k)
+    if kind == "gauss":
+        y = rng.standard_normal((m, k))
+    elif kind == "lowrank":     # exercises the PIVOT_RTOL branch (factor.py:70-75)
+        y = rng.standard_normal((m, 5)) @ rng.standard_normal((5, k))
+    else:                       # many exactly tied pivot candidates
+        y = rng.integers(-3, 4, (m, k)).astype(np.float64)
+    want = O.lu_row_pivot(y)
+    got = O.lu_row_pivot_blocked(y, nthreads=threads)
+    for w, g_ in zip(want, got):
+        np.testing.assert_array_equal(w, g_)
+    c = y[: min(k, 64) + 7].T.copy() if kind == "lowrank" else y[:k].T.copy()  # k' x n
+    want = O.lu_col_pivot(c)
+    got = O.lu_col_pivot_blocked(np.ascontiguousarray(c.T), nthreads=threads)
+    for w, g_ in zip(want, got):
+        np.testing.assert_array_equal(w, g_)
+
+
+def test_chunked_sketches_match_restatement():
+    import scipy.sparse as sp
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((300, 700)).astype(np.float32)
+    om = draws.build_composite(40, 160, 700, 3)
+    np.testing.assert_array_equal(O.sketch_right_rows(a, om, nthreads=3),
+                                  O.apply_sketch_right(O.as_matrix(a.astype(np.float64)), om))
+    s = sp.random(300, 700, density=0.02, random_state=1, format="csr")
+    np.testing.assert_array_equal(O.sketch_right_rows(s, om),
+                                  O.apply_sketch_right(O.as_matrix(s), om))
+    om2 = draws.build_composite(30, 120, 300, 4)
+    perm = rng.permutation(300)
+    for dt in (np.float32, np.float64):
+        got = O.sketch_left_cols(a.astype(dt), perm, om2, nthreads=3)
+        want = O.apply_sketch_left(om2, a.astype(np.float64)[perm])
+        np.testing.assert_array_equal(got, want.T)
