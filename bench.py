@@ -44,7 +44,7 @@ CONFIGS = {
     5: dict(m=65536, n=65536, dtype="f64", k=500, l=550, width=4400, name="dense 65536x65536 fp64, "
             "Haar rank 1000, sigma_i=10^(-4(i-1)/999), + N(0,1e-8) noise (std)"),
 }
-HAAR_RANK_CFG2 = 1024   # sigma_i = i^-2 beyond i=1024 contributes < 2e-5 (noise: 1.6e-2)
+HAAR_RANK_CFG2 = 16384  # full 16384 x 16384 Haar factors, as BASELINE config 2 states
 
 
 def _gen(seed, device):
@@ -59,66 +59,109 @@ def _haar_cols(m, r, g, device):
     return q * torch.sign(torch.diagonal(rr))
 
 
-def gen_config(c, device="cuda"):
+GEN_BLOCK = 4096   # rows per independently seeded block of the generators
+
+
+def _blocks(r0, r1):
+    return range(r0 // GEN_BLOCK, (r1 + GEN_BLOCK - 1) // GEN_BLOCK)
+
+
+def _block_noise(c, b, n, std, device, dtype):
+    """Noise of generator block b (rows [b*GEN_BLOCK, (b+1)*GEN_BLOCK)):
+    its own seed, so any row range is generated identically alone or as
+    part of the whole matrix (row-sharded ranks generate only their rows)."""
+    g = _gen((1000 + c) * 1000003 + b, device)
+    return std * torch.randn(GEN_BLOCK, n, generator=g, device=device, dtype=dtype)
+
+
+def gen_config(c, device="cuda", row_range=None):
     """Synthetic A of BASELINE config c on the device (deterministic per
-    seed) and its RandLuParams fields.  Noise 'N(0,v)' is read as standard
-    deviation v."""
+    seed) and its RandLuParams fields; ``row_range=(r0, r1)`` generates only
+    those rows (the same values as the full matrix's rows: the noise and the
+    row factors are seeded per 4096-row block).  Noise 'N(0,v)' is read as
+    standard deviation v."""
     from paper_1601_04280_b200 import params_from_north_star
     cfg = CONFIGS[c]
     m, n = cfg["m"], cfg["n"]
+    r0, r1 = row_range if row_range is not None else (0, m)
     prm = params_from_north_star(m, n, cfg["k"], cfg["l"], cfg["width"], seed=0)
     prm = dict(r=prm.r, k1=prm.k1, l1=prm.l1, k2=prm.k2, l2=prm.l2, seed=0)
     g = _gen(1000 + c, device)
+
+    def rows_of(fn, dtype):
+        out = []
+        for b in _blocks(r0, r1):
+            blk = fn(b)
+            lo, hi = max(r0, b * GEN_BLOCK), min(r1, (b + 1) * GEN_BLOCK)
+            out.append(blk[lo - b * GEN_BLOCK:hi - b * GEN_BLOCK].to(dtype))
+        return torch.cat(out, 0).contiguous()
+
     if c == 1:
         from tests.golden.cases import config1_matrix
         from threadpoolctl import threadpool_limits
         with threadpool_limits(1):
             a = torch.from_numpy(config1_matrix()).to(device)
-        return a.contiguous(), prm
-    if c == 2:
-        r = HAAR_RANK_CFG2
+        return a[r0:r1].contiguous(), prm
+    if c in (2, 5):
+        # U, V: Haar of rank r (QR of seeded N(0,1) with the sign fix), whole
+        # on every rank (m x r); A rows = U[rows] diag(sigma) V^T + noise
+        r = min(HAAR_RANK_CFG2, m, n) if c == 2 else 1000
         u = _haar_cols(m, r, g, device)
         v = _haar_cols(n, r, g, device)
-        s = torch.arange(1, r + 1, device=device, dtype=torch.float64) ** -2.0
-        a = (u * s) @ v.t()
-        del u, v
-        a += 1e-6 * torch.randn(m, n, generator=g, device=device, dtype=torch.float64)
-        return a.float().contiguous(), prm
+        if c == 2:
+            s = torch.arange(1, r + 1, device=device, dtype=torch.float64) ** -2.0
+            std, dt = 1e-6, torch.float32
+        else:
+            s = 10.0 ** (-4.0 * torch.arange(r, device=device, dtype=torch.float64) / 999.0)
+            std, dt = 1e-8, torch.float64
+        us = u * s
+        del u
+
+        def blk(b):
+            lo = b * GEN_BLOCK
+            x = us[lo:lo + GEN_BLOCK] @ v.t()
+            nz = _block_noise(c, b, n, std, device, torch.float64)
+            x += nz[:x.shape[0]]
+            return x
+
+        return rows_of(blk, dt), prm
     if c == 3:
-        g1 = torch.randn(m, 200, generator=g, device=device) / math.sqrt(200.0)
         g2 = torch.randn(200, n, generator=g, device=device) / math.sqrt(200.0)
-        a = g1 @ g2
-        del g1, g2
-        for r0 in range(0, m, 16384):
-            a[r0:r0 + 16384] += 1e-3 * torch.randn(min(16384, m - r0), n, generator=g,
-                                                   device=device)
-        return a.contiguous(), prm
+
+        def blk(b):
+            gb = _gen((1000 + c) * 1000003 + b, device)
+            g1 = torch.randn(GEN_BLOCK, 200, generator=gb, device=device) / math.sqrt(200.0)
+            x = g1 @ g2
+            x += 1e-3 * torch.randn(GEN_BLOCK, n, generator=gb, device=device)
+            return x
+
+        return rows_of(blk, torch.float32), prm
     if c == 4:
-        nnz = int(round(m * n * 1e-3))
-        rows = torch.randint(0, m, (nnz,), generator=g, device=device)
-        cols = torch.randint(0, n, (nnz,), generator=g, device=device)
-        vals = torch.randn(nnz, generator=g, device=device, dtype=torch.float64)
-        key = rows * n + cols
-        key, order = torch.sort(key)
-        vals = vals[order]
-        uk, inv = torch.unique_consecutive(key, return_inverse=True)
-        sv = torch.zeros(uk.numel(), dtype=torch.float64, device=device).index_add_(0, inv, vals)
-        r = (uk // n)
-        indptr = torch.zeros(m + 1, dtype=torch.int64, device=device)
-        indptr[1:] = torch.cumsum(torch.bincount(r, minlength=m), 0)
-        indices = (uk % n).to(torch.int32)
-        return (indptr, indices, sv.float()), prm
-    if c == 5:
-        r = 1000
-        u = _haar_cols(m, r, g, device)
-        v = _haar_cols(n, r, g, device)
-        s = 10.0 ** (-4.0 * torch.arange(r, device=device, dtype=torch.float64) / 999.0)
-        a = (u * s) @ v.t()
-        del u, v
-        for r0 in range(0, m, 4096):
-            a[r0:r0 + 4096] += 1e-8 * torch.randn(min(4096, m - r0), n, generator=g,
-                                                  device=device, dtype=torch.float64)
-        return a, prm
+        # per 4096-row block: round(4096 n 1e-3) i.i.d. uniform positions in
+        # the block (stratified i.i.d.), values N(0,1), duplicates summed
+        nnz_b = int(round(GEN_BLOCK * n * 1e-3))
+        ptrs, idxs, vals = [torch.zeros(1, dtype=torch.int64, device=device)], [], []
+        base = 0
+        for b in _blocks(r0, r1):
+            gb = _gen((1000 + c) * 1000003 + b, device)
+            rows = torch.randint(0, GEN_BLOCK, (nnz_b,), generator=gb, device=device)
+            cols = torch.randint(0, n, (nnz_b,), generator=gb, device=device)
+            vv = torch.randn(nnz_b, generator=gb, device=device, dtype=torch.float64)
+            lo, hi = max(r0, b * GEN_BLOCK), min(r1, (b + 1) * GEN_BLOCK)
+            keep = (rows >= lo - b * GEN_BLOCK) & (rows < hi - b * GEN_BLOCK)
+            rows, cols, vv = rows[keep] - (lo - b * GEN_BLOCK), cols[keep], vv[keep]
+            key = rows * n + cols
+            key, order = torch.sort(key)
+            vv = vv[order]
+            uk, inv = torch.unique_consecutive(key, return_inverse=True)
+            sv = torch.zeros(uk.numel(), dtype=torch.float64, device=device).index_add_(0, inv, vv)
+            rr = uk // n
+            cnt = torch.bincount(rr, minlength=hi - lo)
+            ptrs.append(base + torch.cumsum(cnt, 0))
+            base += int(uk.numel())
+            idxs.append((uk % n).to(torch.int32))
+            vals.append(sv.float())
+        return (torch.cat(ptrs), torch.cat(idxs), torch.cat(vals)), prm
     raise ValueError(c)
 
 

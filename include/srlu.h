@@ -239,8 +239,10 @@ int srlu_lu_colpiv(double *ct, int64_t n, int64_t k, int64_t ldc, int64_t *q, do
  * pinvT = (R^-1 Q^T)^T (k2 x k1 row-major); the rank test is
  * srlu_qr_rank (stats[4]: sigma_max estimate, sigma_min estimate, cond,
  * singular flag = 1.0 when sigma_min <= 1e-10 sigma_max, factor.py:124).
- * `stats` is unused here (kept for ABI stability).  Needs
- * srlu_qr_pinv_smem_bytes(k1, k2) <= 220 KiB, else SRLU_ERR_UNSUPPORTED. */
+ * `stats` is unused here (kept for ABI stability).  When M does not fit one
+ * CTA (srlu_qr_pinv_smem_bytes(k1, k2) > 220 KiB or k1 > 256) the QR runs
+ * on one thread-block cluster of up to 16 CTAs (k1 <= 576; M's columns
+ * spread over the CTAs' shared memory, reflectors pushed through DSMEM). */
 size_t srlu_qr_pinv_smem_bytes(int64_t k1, int64_t k2);
 size_t srlu_qr_pinv_workspace(int64_t k1, int64_t k2);
 int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *pinvT,
@@ -250,6 +252,24 @@ int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *
  * after srlu_qr_pinv on the same stream; it can overlap later work on
  * other streams: only the host's final decision needs stats). */
 int srlu_qr_rank(const void *ws, int64_t k1, int64_t k2, double *stats, srlu_stream_t stream);
+
+/* srlu_qr_rank plus certified bounds, once pinvT (srlu_qr_pinv's output) is
+ * ready: stats[8] = {sigma_max estimate, sigma_min estimate, cond estimate,
+ * flag, ||R||_F, ||pinv||_F, ||R||_F ||pinv||_F, 0}.  The estimates bracket
+ * the extreme singular values from the inside and ||R||_F, 1/||R^-1||_F =
+ * 1/||pinv||_F from the outside, so flag = 1 (singular: sigma_min <= 1e-10
+ * sigma_max, factor.py:123-124) and flag = 0 (not) are certain; flag = 2:
+ * the bounds straddle the threshold — call srlu_rank_exact. */
+int srlu_qr_rank_certified(const void *ws, int64_t k1, int64_t k2, const double *pinvT,
+                           int64_t ldp, double *stats, srlu_stream_t stream);
+
+/* the reference's decision on the singular values themselves (factor.py:
+ * 122-128 numpy.linalg.svd of R): one-sided Jacobi on the R left in the
+ * srlu_qr_pinv workspace qr_ws; stats[4] = {sigma_max, sigma_min, cond,
+ * singular flag}.  ws: srlu_rank_exact_workspace(k1) bytes. */
+size_t srlu_rank_exact_workspace(int64_t k1);
+int srlu_rank_exact(const void *qr_ws, int64_t k1, int64_t k2, void *ws, size_t ws_bytes,
+                    double *stats, srlu_stream_t stream);
 
 /* the same rank test on an upper-triangular R (k x k, k <= 576, device),
  * given row-major (R, ldr) and transposed (RT = R^T row-major, ldt) */

@@ -73,6 +73,9 @@ SIGNATURES = {
     "srlu_qr_pinv": (INT, [P, I64, I64, I64, P, I64, P, P, SZ, P]),
     "srlu_rank_estimate": (INT, [P, I64, I64, P, I64, P, P]),
     "srlu_qr_rank": (INT, [P, I64, I64, P, P]),
+    "srlu_qr_rank_certified": (INT, [P, I64, I64, P, I64, P, P]),
+    "srlu_rank_exact_workspace": (SZ, [I64]),
+    "srlu_rank_exact": (INT, [P, I64, I64, P, SZ, P, P]),
     "srlu_dgemm": (INT, [P, I64, P, I64, P, I64, I64, I64, I64, P]),
     "srlu_dgemm_ex": (INT, [P, I64, P, I64, P, I64, I64, I64, I64, INT, P]),
     "srlu_lu_error_workspace": (SZ, [I64, I64, I64]),
@@ -126,7 +129,7 @@ class _LaunchCounter:
                 "k1_schedule": 2, "k1_schedule_1": 1, "sketch_right_dense_sched": 1,
                 "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
                 "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 6,
-                "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1,
+                "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1, "rank_exact": 1,
                 "dgemm": 1, "lu_error": 3}
 
     def __init__(self):

@@ -30,6 +30,12 @@ __device__ long long g_qr_trace[256][6];
 
 namespace srlu {
 
+// qr_cluster.cu
+int qr_cluster_launch(const double *mT, int64_t k1, int64_t k2, int64_t ldm, double *qa,
+                      double *qtau, double *rrow, cudaStream_t st);
+size_t jacobi_workspace(int64_t k);
+int jacobi_launch(const double *rrow, int64_t k, void *ws, double *stats, cudaStream_t st);
+
 constexpr double kRankRtol = 1e-10;  // factor.py:22
 
 __device__ inline double block_sum(double v, double *red) {
@@ -177,7 +183,9 @@ __device__ double inverse_iteration(const double *__restrict__ Rr, int64_t ldr,
 
 __device__ void rank_estimate(const double *__restrict__ Rr, int64_t ldr,
                               const double *__restrict__ Rc, int64_t ldc, int k, double *x,
-                              double *y, double *red, double *stats) {
+                              double *y, double *red, double *stats,
+                              const double *__restrict__ pinvT = nullptr, int64_t ldp = 0,
+                              int k2 = 0) {
     const int tid = threadIdx.x;
     double dmax = 0.0, dmin = INFINITY;
     for (int j = tid; j < k; j += blockDim.x) {
@@ -232,11 +240,42 @@ __device__ void rank_estimate(const double *__restrict__ Rr, int64_t ldr,
     } else if (!(dmin > 0.0)) {
         smin = 0.0;
     }
+    // certified bounds (pinvT given): sigma_max <= ||R||_F and sigma_min >=
+    // 1/||R^-1||_F = 1/||pinv||_F (pinv = R^-1 Q^T, Q orthonormal columns)
+    double fr = 0.0, fp = 0.0;
+    if (pinvT != nullptr) {
+        for (int64_t i = tid; i < (int64_t)k * k; i += blockDim.x) {
+            const int r = (int)(i / k), c = (int)(i % k);
+            if (c >= r) {
+                const double v = Rr[(int64_t)r * ldr + c];
+                fr = __fma_rn(v, v, fr);
+            }
+        }
+        for (int64_t i = tid; i < (int64_t)k2 * k; i += blockDim.x) {
+            const double v = pinvT[(i / k) * ldp + i % k];
+            fp = __fma_rn(v, v, fp);
+        }
+        fr = block_sum(fr, red);
+        fp = block_sum(fp, red);
+    }
     if (tid == 0) {
         stats[0] = smax;
         stats[1] = smin;
         stats[2] = smin > 0.0 ? smax / smin : INFINITY;
-        stats[3] = (smax == 0.0 || smin <= kRankRtol * smax) ? 1.0 : 0.0;
+        // estimates bracket from the inside: smin_true <= smin, smax_true >= smax
+        const bool sing = smax == 0.0 || smin <= kRankRtol * smax;
+        stats[3] = sing ? 1.0 : 0.0;
+        if (pinvT != nullptr) {
+            const double hi = sqrt(fr) * sqrt(fp);  // >= the true condition number
+            stats[4] = sqrt(fr);
+            stats[5] = sqrt(fp);
+            stats[6] = hi;
+            stats[7] = 0.0;
+            // certain when the outside bound already clears the threshold
+            // (1e-4 margin: pinv's own rounding at cond <= 1e10), else
+            // flag 2 = undecided: the host runs the exact singular values
+            if (!sing && !(isfinite(hi) && hi * (1.0 + 1e-4) < 1.0 / kRankRtol)) stats[3] = 2.0;
+        }
     }
 }
 
@@ -519,12 +558,14 @@ __global__ void __launch_bounds__(256, 1) rank_estimate_kernel(const double *__r
                                                                       int k, int64_t ldr,
                                                                       const double *__restrict__ RT,
                                                                       int64_t ldt,
-                                                                      double *__restrict__ stats) {
+                                                                      double *__restrict__ stats,
+                                                                      const double *__restrict__ pinvT,
+                                                                      int64_t ldp, int k2) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *xv = reinterpret_cast<double *>(smem_raw);
     double *yv = xv + k;
     double *red = yv + k;
-    rank_estimate(R, ldr, RT, ldt, k, xv, yv, red, stats);
+    rank_estimate(R, ldr, RT, ldt, k, xv, yv, red, stats, pinvT, ldp, k2);
 }
 
 
@@ -828,18 +869,21 @@ extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ld
     SRLU_REQUIRE(ws_bytes >= srlu_qr_pinv_workspace(k1, k2), SRLU_ERR_WORKSPACE,
                  "qr_pinv: workspace too small");
     size_t smem = qr_pinv_smem(k1, k2);
-    SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED,
-                 "qr_pinv: %lld x %lld does not fit one CTA's shared memory", (long long)k2,
-                 (long long)k1);
     cudaStream_t s = (cudaStream_t)stream;
     double *qa = (double *)ws;
     double *qtau = qa + (size_t)k1 * (k2 | 1);
     double *rrow = qtau + k1;
-    {  // one group of 8 (k1 <= 128) or 4 threads per column; register-resident
+    const char *qv = getenv("SRLU_QR");  // testing knob: smem | reg | cluster
+    if (smem > 220 * 1024 || k1 > 256 || (qv && !strcmp(qv, "cluster"))) {
+        // M does not fit one CTA: the cluster QR (qr_cluster.cu)
+        SRLU_REQUIRE(k1 <= 32 * kRankMaxPerLane, SRLU_ERR_UNSUPPORTED, "qr_pinv: k1 > %d",
+                     32 * kRankMaxPerLane);
+        const int rc0 = qr_cluster_launch(mT, k1, k2, ldm, qa, qtau, rrow, s);
+        if (rc0 != SRLU_OK) return rc0;
+    } else {  // one group of 8 (k1 <= 128) or 4 threads per column; register-resident
        // columns when they fit 16 registers per thread
         void (*qr)(const double *, int, int, int64_t, double *, double *, double *) =
             k1 <= 128 ? qr_kernel<8> : qr_kernel<4>;
-        const char *qv = getenv("SRLU_QR");  // testing knob: smem | reg (default: lookahead)
         if (k1 <= 128 && k2 <= 128 && qv && !strcmp(qv, "reg")) qr = qr_reg_kernel<16>;
         else if (k1 * 8 + 32 <= 1024 && !(qv && !strcmp(qv, "smem"))) {
             qr = nullptr;  // qr_la_kernel<8>
@@ -870,12 +914,14 @@ extern "C" int srlu_qr_pinv(const double *mT, int64_t k1, int64_t k2, int64_t ld
         return SRLU_OK;
     };
     int rc;
-    if (k2 <= 32) rc = tail(qr_tail_kernel<1>);
+    if (smem_v > 220 * 1024) rc = SRLU_ERR_UNSUPPORTED;  // reflectors do not fit: any-k2 tail
+    else if (k2 <= 32) rc = tail(qr_tail_kernel<1>);
     else if (k2 <= 64) rc = tail(qr_tail_kernel<2>);
     else if (k2 <= 128) rc = tail(qr_tail_kernel<4>);
     else if (k2 <= 192) rc = tail(qr_tail_kernel<6>);
     else if (k2 <= 32 * kTailMaxPer) rc = tail(qr_tail_kernel<kTailMaxPer>);
-    else {
+    else rc = SRLU_ERR_UNSUPPORTED;
+    if (rc == SRLU_ERR_UNSUPPORTED) {
         const size_t smem2 = sizeof(double) * (size_t)(8 * ((k2 + 1) & ~1) + 64);
         SRLU_REQUIRE(smem2 <= 200 * 1024, SRLU_ERR_UNSUPPORTED, "qr_pinv: k2 too large");
         SRLU_CUDA(cudaFuncSetAttribute(qr_tail_any_kernel,
@@ -901,7 +947,7 @@ extern "C" int srlu_rank_estimate(const double *R, int64_t k, int64_t ldr, const
     SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     rank_estimate_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(R, (int)k, ldr, RT, ldt,
-                                                                         stats);
+                                                                         stats, nullptr, 0, 0);
     SRLU_CHECK_LAUNCH("rank_estimate_kernel");
     return SRLU_OK;
 }
@@ -922,7 +968,40 @@ extern "C" int srlu_qr_rank(const void *ws, int64_t k1, int64_t k2, double *stat
                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     // R row-major = rrow, R column-major = the packed QR (column stride k2|1)
     rank_estimate_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(rrow, (int)k1, k1, qa,
-                                                                 (int64_t)(k2 | 1), stats);
+                                                                 (int64_t)(k2 | 1), stats,
+                                                                 nullptr, 0, 0);
     SRLU_CHECK_LAUNCH("rank_estimate_kernel");
+    return SRLU_OK;
+}
+
+extern "C" int srlu_qr_rank_certified(const void *ws, int64_t k1, int64_t k2, const double *pinvT,
+                                      int64_t ldp, double *stats, srlu_stream_t stream) {
+    SRLU_REQUIRE(k1 >= 1 && k2 >= k1 && k1 <= 32 * kRankMaxPerLane && ldp >= k1 && pinvT,
+                 SRLU_ERR_ARG, "qr_rank: bad sizes");
+    const double *qa = (const double *)ws;
+    const double *rrow = qa + (size_t)k1 * (k2 | 1) + k1;
+    size_t smem = sizeof(double) * (size_t)(2 * k1 + 64);
+    SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SRLU_CUDA(cudaFuncSetAttribute(rank_estimate_kernel,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    rank_estimate_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(rrow, (int)k1, k1, qa,
+                                                                 (int64_t)(k2 | 1), stats,
+                                                                 pinvT, ldp, (int)k2);
+    SRLU_CHECK_LAUNCH("rank_estimate_kernel");
+    return SRLU_OK;
+}
+
+extern "C" size_t srlu_rank_exact_workspace(int64_t k1) { return jacobi_workspace(k1); }
+
+extern "C" int srlu_rank_exact(const void *qr_ws, int64_t k1, int64_t k2, void *ws,
+                               size_t ws_bytes, double *stats, srlu_stream_t stream) {
+    SRLU_REQUIRE(k1 >= 1 && k2 >= k1, SRLU_ERR_ARG, "rank_exact: bad sizes");
+    SRLU_REQUIRE(ws && ws_bytes >= jacobi_workspace(k1), SRLU_ERR_WORKSPACE,
+                 "rank_exact: workspace too small");
+    const double *rrow = (const double *)qr_ws + (size_t)k1 * (k2 | 1) + k1;
+    int rc = jacobi_launch(rrow, k1, ws, stats, (cudaStream_t)stream);
+    if (rc) return rc;
+    SRLU_CHECK_LAUNCH("jacobi_sv_kernel");
     return SRLU_OK;
 }

@@ -107,46 +107,50 @@ def lu_col_pivot(mat) -> ColPivotedLU:
                         Matrix.from_device(ut.t().contiguous()))
 
 
-QR_SMEM_LIMIT = 220 * 1024
+class RankTest:
+    """Device state of one rank test (factor.py:122-128): the certified
+    stats[8] of srlu_qr_rank_certified and the QR workspace (R) for the
+    exact fallback."""
+
+    __slots__ = ("stats", "ws", "k1", "k2")
+
+    def __init__(self, stats, ws, k1, k2):
+        self.stats, self.ws, self.k1, self.k2 = stats, ws, k1, k2
+
+    def record_stream(self, stream):
+        self.stats.record_stream(stream)
+        self.ws.record_stream(stream)
 
 
 def pinv_dev(m_t: torch.Tensor, stream=None, rank_event=False):
     """pinv of M = m_t^T (k2 x k1) on the device (factor.py:112-130).
-    ``m_t``: k1 x k2 row-major fp64.  Returns (pinvT k2 x k1, stats[4]
-    device: sigma_max, sigma_min estimates, cond, singular flag[, event]).
-    The rank test is enqueued AFTER the pinv (same stream) so a consumer of
-    pinvT can wait on the returned event and overlap the rank test; the
-    caller decides singularity after its one host sync.  One CTA of libsrlu
-    does the Householder QR when M fits in shared memory; otherwise the QR
-    comes from cuSOLVER and the rank test from libsrlu."""
+    ``m_t``: k1 x k2 row-major fp64.  Returns (pinvT k2 x k1, RankTest[,
+    event]).  The rank test is enqueued AFTER the pinv (same stream) so a
+    consumer of pinvT can wait on the returned event and overlap the rank
+    test; the caller decides singularity after its one host sync
+    (``check_rank``).  libsrlu's Householder QR runs in one CTA when M fits
+    its shared memory, else on one thread-block cluster (k1 <= 576)."""
     L = _lib.lib()
     m_t = m_t.contiguous()
     k1, k2 = m_t.shape
     if k2 < k1:
         raise ShapeError(f"need rows >= cols, got {k2} x {k1}")
     dev = m_t.device
-    stats = torch.empty(4, dtype=torch.float64, device=dev)
+    stats = torch.empty(8, dtype=torch.float64, device=dev)
     sh = _lib.stream_handle(stream)
     ev = torch.cuda.Event()
-    if L.srlu_qr_pinv_smem_bytes(k1, k2) <= QR_SMEM_LIMIT:
-        pinv_t = torch.empty(k2, k1, dtype=torch.float64, device=dev)
-        ws = _lib.workspace(L.srlu_qr_pinv_workspace(k1, k2), dev)
-        _lib.check(L.srlu_qr_pinv(_lib.ptr(m_t), k1, k2, m_t.stride(0), _lib.ptr(pinv_t),
-                                  pinv_t.stride(0), _lib.ptr(stats), _lib.ptr(ws), ws.numel(), sh),
-                   "qr_pinv")
-        ev.record(stream)
-        _lib.check(L.srlu_qr_rank(_lib.ptr(ws), k1, k2, _lib.ptr(stats), sh), "qr_rank")
-    else:
-        qf, rf = torch.linalg.qr(m_t.t(), mode="reduced")
-        rf = rf.contiguous()
-        pinv_t = torch.linalg.solve_triangular(rf, qf.t().contiguous(), upper=True).t().contiguous()
-        ev.record(stream)
-        rft = rf.t().contiguous()
-        _lib.check(L.srlu_rank_estimate(_lib.ptr(rf), k1, rf.stride(0), _lib.ptr(rft),
-                                        rft.stride(0), _lib.ptr(stats), sh), "rank_estimate")
+    pinv_t = torch.empty(k2, k1, dtype=torch.float64, device=dev)
+    ws = _lib.workspace(L.srlu_qr_pinv_workspace(k1, k2), dev)
+    _lib.check(L.srlu_qr_pinv(_lib.ptr(m_t), k1, k2, m_t.stride(0), _lib.ptr(pinv_t),
+                              pinv_t.stride(0), _lib.ptr(stats), _lib.ptr(ws), ws.numel(), sh),
+               "qr_pinv")
+    ev.record(stream)
+    _lib.check(L.srlu_qr_rank_certified(_lib.ptr(ws), k1, k2, _lib.ptr(pinv_t), pinv_t.stride(0),
+                                        _lib.ptr(stats), sh), "qr_rank")
+    rt = RankTest(stats, ws, k1, k2)
     if rank_event:
-        return pinv_t, stats, ev
-    return pinv_t, stats
+        return pinv_t, rt, ev
+    return pinv_t, rt
 
 
 def dgemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, stream=None,
@@ -172,13 +176,31 @@ def dgemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, str
     return out
 
 
-def check_rank(stats_host):
-    """factor.py:123-128 on the estimates from pinv_dev."""
-    smax, smin, cond, singular = (float(x) for x in stats_host)
+def check_rank(stats_host, rank: RankTest | None = None, stream=None):
+    """factor.py:123-128 on the certified bounds of srlu_qr_rank_certified;
+    undecided (flag 2: the bounds straddle 1e-10) -> the singular values of
+    R themselves (srlu_rank_exact, one-sided Jacobi on the device), like the
+    reference.  Returns the stats the decision was made on."""
+    st = [float(x) for x in stats_host]
+    if st[3] == 2.0:
+        if rank is None:
+            raise RuntimeError("undecided rank test needs the device R")
+        L = _lib.lib()
+        dev = rank.ws.device
+        ex = torch.empty(4, dtype=torch.float64, device=dev)
+        ws = _lib.workspace(L.srlu_rank_exact_workspace(rank.k1), dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        _lib.check(L.srlu_rank_exact(_lib.ptr(rank.ws), rank.k1, rank.k2, _lib.ptr(ws),
+                                     ws.numel(), _lib.ptr(ex), _lib.stream_handle(s)),
+                   "rank_exact")
+        st = [float(x) for x in ex.cpu()] + [0.0] * 4
+        st[7] = 1.0   # decided on the exact singular values
+    smax, smin, cond, singular = st[:4]
     if singular:
         cond = float("inf") if smin == 0.0 else float(smax / smin)
         raise SingularMatrixError(
             f"matrix is numerically rank deficient (condition estimate {cond:.3e})", cond=cond)
+    return st
 
 
 def left_pseudo_inverse(mat) -> Matrix:
@@ -187,6 +209,6 @@ def left_pseudo_inverse(mat) -> Matrix:
     p, q = m.shape
     if p < q:
         raise ShapeError(f"need rows >= cols, got {p} x {q}")
-    pinv_t, stats = pinv_dev(m.t().contiguous())
-    check_rank(stats.cpu().numpy())
+    pinv_t, rt = pinv_dev(m.t().contiguous())
+    check_rank(rt.stats.cpu().numpy(), rt)
     return Matrix.from_device(pinv_t.t().contiguous())

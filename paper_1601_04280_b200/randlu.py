@@ -207,7 +207,7 @@ def _attempt_gaussian(a: Matrix, params: RandLuParams, attempt: int, keep: bool)
     red_aT = (a_op.t() @ g2p.t()).contiguous() if a.is_sparse else \
         (a_op.t() @ g2p.t()).contiguous()                  # (G2 P A)^T, n x k2
     ev[3].record(main)
-    pinv_t, stats = pinv_dev(red_lT)
+    pinv_t, rank = pinv_dev(red_lT)
     core_t = dgemm(red_aT, pinv_t)
     ev[4].record(main)
     core_keep = core_t.clone() if keep else None
@@ -215,7 +215,7 @@ def _attempt_gaussian(a: Matrix, params: RandLuParams, attempt: int, keep: bool)
     l_final = dgemm(l1, lt, b_lower=True)
     ev[5].record(main)
     ev[5].synchronize()
-    check_rank(stats.cpu().numpy())
+    check_rank(rank.stats.cpu().numpy(), rank)
     elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
     res = RandLuResult(P=Permutation(perm.cpu().numpy(), perm, validate=False),
                        Q=Permutation(q.cpu().numpy(), q, validate=False),
@@ -353,9 +353,10 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     with torch.cuda.stream(side):
         # pinv first; the rank test follows on the side stream and overlaps
         # the core GEMM and K5 (only the final host decision needs it)
-        pinv_t, stats, ev_pinv = pinv_dev(red_lT, stream=side, rank_event=True)
+        pinv_t, rank, ev_pinv = pinv_dev(red_lT, stream=side, rank_event=True)
     pinv_t.record_stream(main)
-    stats.record_stream(main)
+    rank.record_stream(main)
+    stats = rank.stats
     red_lT.record_stream(side)
     red_aT = torch.empty(n, k2, dtype=torch.float64, device=dev)
     if a.is_sparse:
@@ -388,8 +389,7 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
         raise ValueError("matrix entries must be finite")
     if fl & 2:
         raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
-    stats_host = stats_h.numpy()
-    check_rank(stats_host)
+    stats_host = check_rank(stats_h.numpy(), rank)
     elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
     res = RandLuResult(P=Permutation(perm_h.numpy(), perm, validate=False),
                        Q=Permutation(q_h.numpy(), q, validate=False),

@@ -39,19 +39,45 @@ class OracleOps:
         red = O.apply_sketch_left(om2, pa)          # k2 x n
         return torch.from_numpy(np.ascontiguousarray(red.T))
 
-    def tail(self, l1, om2, red_aT, params):
+    def pinv_async(self, l1, om2, params):
         red_l = O.apply_sketch_left(om2, l1.numpy())
         try:
-            pinv = O.left_pseudo_inverse(red_l)
+            return torch.from_numpy(np.ascontiguousarray(O.left_pseudo_inverse(red_l).T)), None
         except O.SingularMatrixError as e:
-            k1 = l1.shape[1]
-            z = torch.zeros(1)
-            return (torch.arange(red_aT.shape[0]), l1, torch.zeros(red_aT.shape[0], k1),
-                    np.array([1.0, 0.0, e.cond, 1.0]))
-        core = O.matmul(pinv, red_aT.numpy().T)
-        q, lt, u = O.lu_col_pivot(core)
+            return torch.zeros(params.k2, params.k1, dtype=torch.float64), e
+
+    def pinv_wait(self, handle):
+        return handle
+
+    def decide(self, state):
+        return (True, state.cond) if state is not None else (False, 1.0)
+
+    def gemm(self, a, b):
+        return torch.from_numpy(np.ascontiguousarray(a.numpy() @ b.numpy()))
+
+    def tail(self, l1, core_t):
+        q, lt, u = O.lu_col_pivot(core_t.numpy().T)
         return (torch.from_numpy(q.astype(np.int64)), torch.from_numpy(O.matmul(l1.numpy(), lt)),
-                torch.from_numpy(np.ascontiguousarray(u.T)), np.array([1.0, 1.0, 1.0, 0.0]))
+                torch.from_numpy(np.ascontiguousarray(u.T)))
+
+
+class FlagOps(OracleOps):
+    """Injects K1/K3 status bits on chosen ranks (non-finite entry in one
+    shard, an over-long CSR column in another)."""
+
+    def __init__(self, rank, nonfinite_rank=None, longcol_rank=None):
+        self.rank, self.nf, self.lc = rank, nonfinite_rank, longcol_rank
+
+    def sketch_right(self, a_local, n, params, seed):
+        y, flag = super().sketch_right(a_local, n, params, seed)
+        if self.rank == self.nf:
+            flag[0] |= 1
+        return y, flag
+
+    def sketch_left_partial(self, a_local, row0, om2, perm, n, params, flag):
+        if self.rank == self.lc:
+            flag[0] |= 2
+        return super().sketch_left_partial(a_local, row0, om2, perm, n, params, flag)
 
 
 def _free_port():
@@ -62,7 +88,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, a, prm, out):
+def _worker(rank, world, port, a, prm, out, flags=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -72,7 +98,12 @@ def _worker(rank, world, port, a, prm, out):
         row0, rows = shard_bounds(m, world, rank)
         a_local = Matrix(np.ascontiguousarray(a[row0:row0 + rows]), device="cpu",
                          check_finite=False)
-        res = sparse_randomized_lu_dist(a_local, m, RandLuParams(**prm), ops=OracleOps())
+        ops = OracleOps() if flags is None else FlagOps(rank, **flags)
+        try:
+            res = sparse_randomized_lu_dist(a_local, m, RandLuParams(**prm), ops=ops)
+        except (ValueError, NotImplementedError) as e:
+            out.put((rank, type(e).__name__))
+            return
         if rank == 0:
             out.put(dict(P=res.P.indices.copy(), Q=res.Q.indices.copy(),
                          L=res.L.raw.numpy().copy(), U=res.U.raw.numpy().copy(),
@@ -83,14 +114,16 @@ def _worker(rank, world, port, a, prm, out):
         dist.destroy_process_group()
 
 
-def _run(world, a, prm):
+def _run(world, a, prm, flags=None, nres=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, a, prm, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, a, prm, q, flags))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = q.get(timeout=300)
+    res = [q.get(timeout=300) for _ in range(nres)]
+    res = res[0] if nres == 1 else res
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -127,3 +160,20 @@ def test_row_sharded_resample_lockstep():
     a, prm = cases.pipeline_cases()["lowrank_resample"]
     got = _run(2, a, prm)
     assert got["attempt"] == 2
+
+
+@pytest.mark.parametrize("flags,expect", [
+    (dict(nonfinite_rank=1, longcol_rank=0), "ValueError"),      # bit 0 not masked by bit 1
+    (dict(nonfinite_rank=None, longcol_rank=1), "NotImplementedError"),
+    (dict(nonfinite_rank=2, longcol_rank=None), "ValueError"),
+])
+def test_status_bits_merged_bitwise_all_ranks_raise(flags, expect):
+    """dist.py merges the K1/K3 status bits per bit (MAX of 0/1 vectors):
+    a non-finite entry in one shard and an over-long CSR column in another
+    both reach every rank, and every rank raises the same error."""
+    from tests.golden.cases import gen_rank_noise
+    a = gen_rank_noise(240, 150, 6, 1e-3, 2)
+    prm = dict(r=6, k1=12, l1=48, k2=20, l2=80, seed=1)
+    got = _run(3, a, prm, flags=flags, nres=3)
+    assert sorted(r for r, _ in got) == [0, 1, 2]
+    assert all(name == expect for _, name in got), got
