@@ -197,8 +197,10 @@ int srlu_sem_scatter_dense(const void *a, int dtype, int64_t rows, int64_t n, in
                            srlu_stream_t stream);
 
 /* CSR variant; inv_perm[row] = PA index of local row (row0 offset applied
- * by the caller), row_of2/sign2 indexed by PA index.  *flags |= 2 if a
- * column holds more nonzeros than one CTA sorts in shared memory (8192). */
+ * by the caller), row_of2/sign2 indexed by PA index.  Any column length
+ * (columns beyond one CTA's 8192-entry sort are folded in bucket ranges and
+ * ascending-q chunks); *flags |= 2 is kept for an internal inconsistency
+ * only. */
 size_t srlu_sketch_left_csr_workspace(int64_t rows, int64_t n, int64_t nnz, int64_t l2,
                                       int64_t pad2);
 int srlu_sketch_left_csr(const int64_t *indptr, const int32_t *indices, const void *vals,

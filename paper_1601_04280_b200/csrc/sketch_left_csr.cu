@@ -9,7 +9,8 @@
 // CTA per column then sorts its segment by key in shared memory (bitonic),
 // folds each bucket's run in ascending q (bit-identical sums), applies
 // +-phase, the radix-2 FWHT over pad2 and the k2-row subsample, and writes
-// row j of (Omega2 P A)^T.  P·A is never formed.
+// row j of (Omega2 P A)^T.  P·A is never formed.  Columns longer than one
+// CTA's sort capacity are processed in bucket ranges (any length).
 #include "fwht.cuh"
 #include "fwht_warp.cuh"
 
@@ -185,7 +186,47 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
     }
 }
 
-// One CTA per column (grid-stride); handles columns with lo < count <= CAP.
+// One CTA per column (grid-stride); handles columns with more than lo
+// entries.  A column of at most CAP entries is sorted by key (t, q) in
+// shared memory (bitonic) and each bucket's run folded in ascending q.  A
+// longer column is split by bucket ranges: its bucket histogram (shared
+// memory) is cut into ranges of at most CAP entries, and for each range the
+// CTA re-reads the column's segment, keeps the entries of that range, sorts
+// and folds them.  A single bucket with more than CAP entries (a column
+// denser than CAP x l2) is folded in ascending-q chunks of at most CAP
+// (each chunk's upper q bound found by bisection over q), the running sum
+// carried from chunk to chunk — the reference's one sequential sum.  Any
+// column length, the same per-bucket sums.
+template <int CAP>
+__device__ void csr_sort_fold(unsigned long long *sk, double *sv, int cnt) {
+    int n2 = 1;
+    while (n2 < cnt) n2 <<= 1;
+    for (int i = cnt + threadIdx.x; i < n2; i += blockDim.x) {
+        sk[i] = ~0ULL;
+        sv[i] = 0.0;
+    }
+    __syncthreads();
+    for (int kk = 2; kk <= n2; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ jj;
+                if (ixj > i) {
+                    const bool up = (i & kk) == 0;
+                    const unsigned long long a = sk[i], b = sk[ixj];
+                    if ((a > b) == up) {
+                        sk[i] = b;
+                        sk[ixj] = a;
+                        const double tv = sv[i];
+                        sv[i] = sv[ixj];
+                        sv[ixj] = tv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 template <int CAP>
 __global__ void __launch_bounds__(256) csr_col_project_kernel(
     const int64_t *__restrict__ colptr, const void *__restrict__ ent, const int *__restrict__ modep,
@@ -198,6 +239,11 @@ __global__ void __launch_bounds__(256) csr_col_project_kernel(
     double *x = reinterpret_cast<double *>(smem_raw);                          // pad
     unsigned long long *sk = reinterpret_cast<unsigned long long *>(x + pad);  // CAP
     double *sv = reinterpret_cast<double *>(sk + CAP);                         // CAP
+    int *hist = reinterpret_cast<int *>(sv + CAP);                             // l + 1
+    __shared__ int s_nr, s_fill, s_cnt;
+    __shared__ int s_rb[257];      // range boundaries (a batch of up to 256 ranges)
+    __shared__ unsigned char s_big[256];
+    __shared__ double s_acc;
     const bool reg = pad >= 32;
     const int bsize = pad < 512 ? pad : 512;
     const int nb = pad / bsize;
@@ -205,57 +251,145 @@ __global__ void __launch_bounds__(256) csr_col_project_kernel(
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
         const int64_t p0 = colptr[j];
-        const int cnt = (int)(colptr[j + 1] - p0);
-        if (cnt <= lo) continue;  // handled by the smaller-capacity launch (uniform)
-        if (cnt > CAP) {  // longer columns: next launch, or unsupported in the last one
-            if (flags != nullptr && threadIdx.x == 0) atomicOr(flags, 2);
-            continue;
-        }
+        const int64_t cnt64 = colptr[j + 1] - p0;
+        if (cnt64 <= lo) continue;  // handled by the smaller-capacity launch (uniform)
         for (int t = threadIdx.x; t < pad; t += blockDim.x) x[t] = 0.0;
-        int n2 = 1;
-        while (n2 < cnt) n2 <<= 1;
-        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-            if (i < cnt) {
+        const bool longcol = cnt64 > CAP;
+        if (longcol)
+            for (int t = threadIdx.x; t <= l; t += blockDim.x) hist[t] = 0;
+        __syncthreads();
+        if (longcol) {
+            for (int64_t i = threadIdx.x; i < cnt64; i += blockDim.x) {
                 unsigned t;
                 int q;
                 double v;
                 ent_read(ent, p0 + i, mode, t, q, v);
-                sk[i] = ((unsigned long long)t << 32) | (unsigned)q;
-                sv[i] = v;
-            } else {
-                sk[i] = ~0ULL;
-                sv[i] = 0.0;
+                atomicAdd(hist + t, 1);
             }
+            __syncthreads();
         }
-        __syncthreads();
-        for (int kk = 2; kk <= n2; kk <<= 1) {
-            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-                for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                    const int ixj = i ^ jj;
-                    if (ixj > i) {
-                        const bool up = (i & kk) == 0;
-                        const unsigned long long a = sk[i], b = sk[ixj];
-                        if ((a > b) == up) {
-                            sk[i] = b;
-                            sk[ixj] = a;
-                            const double tv = sv[i];
-                            sv[i] = sv[ixj];
-                            sv[ixj] = tv;
+        int tstart = 0;  // first bucket not yet folded
+        while (tstart < l) {
+            if (threadIdx.x == 0) {
+                int nr = 0, t = tstart;
+                if (!longcol) {
+                    s_rb[0] = 0;
+                    s_rb[1] = l;
+                    s_big[0] = 0;
+                    nr = 1;
+                } else {
+                    s_rb[0] = t;
+                    while (t < l && nr < 256) {
+                        int acc = 0;
+                        const int t0 = t;
+                        while (t < l && acc + hist[t] <= CAP) acc += hist[t++];
+                        s_big[nr] = 0;
+                        if (t == t0) {  // bucket t alone exceeds CAP
+                            s_big[nr] = 1;
+                            ++t;
                         }
+                        s_rb[++nr] = t;
                     }
                 }
+                s_nr = nr;
+            }
+            __syncthreads();
+            const int nr = s_nr;
+            for (int r = 0; r < nr; ++r) {
+                const unsigned t0 = (unsigned)s_rb[r], t1 = (unsigned)s_rb[r + 1];
+                if (!s_big[r]) {
+                    if (threadIdx.x == 0) s_fill = 0;
+                    __syncthreads();
+                    // gather the range's entries (all of them for a short column)
+                    for (int64_t i = threadIdx.x; i < cnt64; i += blockDim.x) {
+                        unsigned t;
+                        int q;
+                        double v;
+                        ent_read(ent, p0 + i, mode, t, q, v);
+                        if (t >= t0 && t < t1) {
+                            const int e = longcol ? atomicAdd(&s_fill, 1) : (int)i;
+                            sk[e] = ((unsigned long long)t << 32) | (unsigned)q;
+                            sv[e] = v;
+                        }
+                    }
+                    __syncthreads();
+                    const int cnt = longcol ? s_fill : (int)cnt64;
+                    csr_sort_fold<CAP>(sk, sv, cnt);
+                    // fold each bucket's run in ascending q (reference order)
+                    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+                        const unsigned t = (unsigned)(sk[i] >> 32);
+                        if (i > 0 && (unsigned)(sk[i - 1] >> 32) == t) continue;
+                        double acc = 0.0;
+                        for (int e = i; e < cnt && (unsigned)(sk[e] >> 32) == t; ++e)
+                            acc = __dadd_rn(acc, sv[e]);
+                        x[reg ? fwht_sw((int)t) : (int)t] = phase[t] < 0.0 ? -acc : acc;
+                    }
+                    __syncthreads();
+                    continue;
+                }
+                // one oversized bucket t0: ascending-q chunks of <= CAP entries
+                int remaining = hist[t0];
+                long long qlast = -1;
+                if (threadIdx.x == 0) s_acc = 0.0;
+                while (remaining > 0) {
+                    long long qhi = 0x7fffffffLL;
+                    if (remaining > CAP) {  // largest qhi with count(qlast < q <= qhi) <= CAP
+                        long long a = qlast, b = 0x7fffffffLL;
+                        while (b - a > 1) {
+                            const long long mid = a + (b - a) / 2;
+                            if (threadIdx.x == 0) s_cnt = 0;
+                            __syncthreads();
+                            int c = 0;
+                            for (int64_t i = threadIdx.x; i < cnt64; i += blockDim.x) {
+                                unsigned t;
+                                int q;
+                                double v;
+                                ent_read(ent, p0 + i, mode, t, q, v);
+                                c += (t == t0 && q > qlast && q <= mid);
+                            }
+                            atomicAdd(&s_cnt, c);
+                            __syncthreads();
+                            if (s_cnt <= CAP) a = mid; else b = mid;
+                            __syncthreads();
+                        }
+                        qhi = a;
+                    }
+                    if (threadIdx.x == 0) s_fill = 0;
+                    __syncthreads();
+                    for (int64_t i = threadIdx.x; i < cnt64; i += blockDim.x) {
+                        unsigned t;
+                        int q;
+                        double v;
+                        ent_read(ent, p0 + i, mode, t, q, v);
+                        if (t == t0 && q > qlast && q <= qhi) {
+                            const int e = atomicAdd(&s_fill, 1);
+                            sk[e] = ((unsigned long long)t << 32) | (unsigned)q;
+                            sv[e] = v;
+                        }
+                    }
+                    __syncthreads();
+                    const int cnt = s_fill;
+                    csr_sort_fold<CAP>(sk, sv, cnt);
+                    if (threadIdx.x == 0) {
+                        double acc = s_acc;
+                        for (int e = 0; e < cnt; ++e) acc = __dadd_rn(acc, sv[e]);
+                        s_acc = acc;
+                    }
+                    __syncthreads();
+                    remaining -= cnt;
+                    qlast = qhi;
+                    if (cnt == 0) {  // cannot happen (the bucket has entries above qlast)
+                        if (flags != nullptr && threadIdx.x == 0) atomicOr(flags, 2);
+                        break;
+                    }
+                }
+                if (threadIdx.x == 0)
+                    x[reg ? fwht_sw((int)t0) : (int)t0] = phase[t0] < 0.0 ? -s_acc : s_acc;
                 __syncthreads();
             }
+            tstart = s_rb[nr];
+            __syncthreads();
         }
-        // fold each bucket's run in ascending q (reference order)
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const unsigned t = (unsigned)(sk[i] >> 32);
-            if (i > 0 && (unsigned)(sk[i - 1] >> 32) == t) continue;
-            double acc = 0.0;
-            for (int e = i; e < cnt && (unsigned)(sk[e] >> 32) == t; ++e) acc = __dadd_rn(acc, sv[e]);
-            x[reg ? fwht_sw((int)t) : (int)t] = phase[t] < 0.0 ? -acc : acc;
-        }
-        __syncthreads();
         if (reg) {
             for (int b = warp; b < nzb; b += blockDim.x >> 5)
                 fwht_block_warp_dyn512(x + b * bsize, bsize, lane);
@@ -444,7 +578,7 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         SRLU_CHECK_LAUNCH("csr_fill_kernel");
     }
     // columns with <= 2048 entries: bucket counting sort (high occupancy);
-    // longer ones (<= 8192) in a bitonic launch; longer still -> flags |= 2
+    // longer ones in a bitonic launch (bucket ranges of <= 8192 entries)
     const int64_t grid = n < 148 * 16 ? n : 148 * 16;
     {
         constexpr int CAP = 2048;
@@ -468,7 +602,8 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         SRLU_CHECK_LAUNCH("csr_col_bucket_kernel");
     }
     {
-        size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * kCsrColCap;
+        size_t smem = sizeof(double) * pad2 + (sizeof(unsigned long long) + sizeof(double)) * kCsrColCap +
+                      sizeof(int) * (l2 + 1);
         SRLU_REQUIRE(smem <= 220 * 1024, SRLU_ERR_UNSUPPORTED, "sketch_left_csr: pad2 too large");
         SRLU_CUDA(cudaFuncSetAttribute(csr_col_project_kernel<kCsrColCap>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

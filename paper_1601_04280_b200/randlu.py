@@ -388,7 +388,7 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     if fl & 1:
         raise ValueError("matrix entries must be finite")
     if fl & 2:
-        raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
+        raise NotImplementedError("sketch_left_csr: a (column, bucket) group exceeds 8192 nonzeros")
     stats_host = check_rank(stats_h.numpy(), rank)
     elapsed = {name: ev[i].elapsed_time(ev[i + 1]) / 1e3 for i, name in enumerate(STAGES)}
     res = RandLuResult(P=Permutation(perm_h.numpy(), perm, validate=False),

@@ -471,7 +471,7 @@ def apply_sketch_left(omega: CompositeSketch, a, perm=None) -> Matrix:
         flags = torch.zeros(1, dtype=torch.int32, device=a.device)
         sketch_left_into(a, omega, None, None, None, outT, inv_perm=inv, flags=flags)
         if int(flags.item()) & 2:
-            raise NotImplementedError("sketch_left_csr: a column exceeds 8192 nonzeros")
+            raise NotImplementedError("sketch_left_csr: a (column, bucket) group exceeds 8192 nonzeros")
     else:
         mrow, msign, bptr = members(omega, pd, 0, a.rows)
         sketch_left_into(a, omega, mrow, msign, bptr, outT)

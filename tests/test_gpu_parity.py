@@ -352,6 +352,45 @@ def test_csr_long_columns_bit_exact(P, dt):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_csr_very_long_columns_bit_exact(P, dt):
+    """Columns far beyond one CTA's 8192-entry sort (50k entries, a dense
+    60k column): bucket-range passes, bit-exact (_fast.pyx:81-90 order)."""
+    from scipy.sparse import csr_array
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(41))
+    m, n = 60000, 200
+    d = g.standard_normal((m, n))
+    d[g.random((m, n)) < 0.995] = 0.0
+    d[g.permutation(m)[:50000], 5] = g.standard_normal(50000)   # a 50k-nnz column
+    d[:, 9] = g.standard_normal(m)                               # a dense column
+    d = d.astype(dt)
+    prm = dict(r=6, k1=14, l1=56, k2=22, l2=88, seed=5)
+    res = P.sparse_randomized_lu(P.Matrix.sparse(csr_array(d)), P.RandLuParams(**prm), keep=True)
+    ref = O.sparse_randomized_lu(csr_array(d), prm, keep=True)
+    np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
+    np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
+
+
+def test_csr_oversized_bucket_group_bit_exact(P):
+    """4 stage-2 buckets and a dense 40k column: ~10k entries of one column
+    in one bucket (> 8192) are folded in ascending-q chunks with the running
+    sum carried over — still the reference's sequential sum."""
+    from scipy.sparse import csr_array
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(43))
+    m, n = 40000, 24
+    d = g.standard_normal((m, n)) * np.exp2(g.integers(-20, 20, size=(m, n)))
+    d[g.random((m, n)) < 0.9] = 0.0
+    d[:, 3] = g.standard_normal(m)
+    prm = dict(r=1, k1=2, l1=8, k2=3, l2=4, seed=2)
+    res = P.sparse_randomized_lu(P.Matrix.sparse(csr_array(d)), P.RandLuParams(**prm), keep=True)
+    ref = O.sparse_randomized_lu(csr_array(d), prm, keep=True)
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
+    np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 def test_csr_crowded_buckets_bit_exact(P, dt):
     """Few stage-2 buckets, ~1600 entries per column: long same-bucket runs whose
     fold order (ascending PA row) matters; values span many binades."""
