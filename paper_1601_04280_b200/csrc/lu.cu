@@ -92,6 +92,7 @@ struct LuParams {
     double *piv;      // [k][k] trailing parts of pivot entities
     double *gpanel;   // GB > 0: attribute-major panel [GB][ldp] (L2-resident)
     int64_t ldp;
+    int l2pf;         // trailing update: L2 prefetch distance in warp passes (0 = off)
 };
 
 __device__ inline bool better(unsigned long long a_abs, unsigned a_pos, unsigned long long b_abs,
@@ -504,6 +505,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                     __syncthreads();
                 }
             }
+            LU_T(4);  // trace: staging + pivot-row recurrence of this chunk
             // rows by warp (RPW per pass), columns by lane (up to two per
             // lane): coalesced, division-free; the next pass's loads are
             // issued before this pass's arithmetic (software pipeline)
@@ -529,9 +531,27 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                     }
                 };
                 int eb = warp * RPW;
+                // L2 prefetch distance (warp passes): the rows' loads hit L2
+                // instead of HBM without holding registers (testing knob
+                // SRLU_LU_L2PF, 0 = off)
+                const int l2pf = GB ? 0 : p.l2pf;  // measured: helps the smem panel only
+                auto prefetch = [&](int ebp) {
+                    if (lane < RPW) {
+                        const int e = ebp + lane;
+                        if (e < ne && pos[e] >= J + bw) {
+                            const uintptr_t a0 = (uintptr_t)(p.w + (e0 + e) * p.ld + x0);
+                            const uintptr_t lo = a0 & ~(uintptr_t)15;
+                            const uintptr_t hi = (a0 + (uintptr_t)xc * 8 + 15) & ~(uintptr_t)15;
+                            bulk_prefetch_l2((const void *)lo, (unsigned)(hi - lo));
+                        }
+                    }
+                };
+                if (l2pf > 0)
+                    for (int d = 1; d <= l2pf; ++d) prefetch(eb + d * stride);
                 if (eb < ne) fetch(eb, vn, pmn, ln);
                 if (SRLU_LU_PFD > 1 && eb + stride < ne) fetch(eb + stride, vn2, pmn2, ln2);
                 for (; eb < ne; eb += stride) {
+                    if (l2pf > 0) prefetch(eb + (l2pf + 1) * stride);
                     double v[RPW][2];
                     double pm[RPW];
                     bool live[RPW];
@@ -601,6 +621,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 }
             }
             __syncthreads();
+            LU_T(5);  // trace: the rows' trailing update of this chunk
         }
     }
 
@@ -2341,6 +2362,8 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     prm.piv = prm.candrow + (size_t)2 * kLuMaxGrid * k;
     prm.gpanel = nullptr;
     prm.ldp = 0;
+    prm.l2pf = 1;  // tools/lu_sweep.sh: config 3 LU(Y) 4.39 -> 4.08 ms
+    if (const char *env = getenv("SRLU_LU_L2PF")) prm.l2pf = atoi(env);  // testing knob
 
     int rc = try_run_lu_hybrid<MODE>(prm, ws, stream);
     if (rc <= 0) return rc;  // launched (0) or failed (<0)
