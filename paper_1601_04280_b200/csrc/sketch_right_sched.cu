@@ -744,9 +744,24 @@ using namespace srlu;
 
 static int es_of(int dtype) { return dtype == SRLU_F32 ? 4 : (dtype == SRLU_F64 ? 8 : 0); }
 
+// sketch_right_tmem.cu: the TMEM-accumulator kernel takes over whenever its
+// geometry applies (128 <= pad1 <= 1024); same plan buffer protocol
+size_t srlu_k1t_plan_bytes(int64_t n, int64_t l1, int64_t pad1, int es);
+int srlu_k1t_info(int64_t n, int64_t l1, int64_t pad1, int es, int64_t info[8]);
+int srlu_k1t_plan(const int32_t *sorted1, const int32_t *bptr1, int64_t n, int64_t l1,
+                  int64_t pad1, int es, void *plan, size_t plan_bytes, cudaStream_t s);
+int srlu_k1t_run(const void *a, int es, int64_t m, int64_t n, int64_t lda, const void *plan,
+                 size_t plan_bytes, int64_t l1, const double *phase1, const int32_t *idx1,
+                 int64_t k1, int64_t pad1, double mult1, double *y, int64_t ldy, int *nonfinite,
+                 cudaStream_t s);
+
 extern "C" size_t srlu_k1_schedule_bytes(int64_t n, int64_t l1, int64_t pad1, int dtype) {
     const int es = es_of(dtype);
     k1s::Cfg f;
+    if (es) {
+        const size_t tb = srlu_k1t_plan_bytes(n, l1, pad1, es);
+        if (tb) return tb;
+    }
     if (!es || !k1s::config(n, l1, pad1, es, &f)) return 0;
     return (size_t)f.ws_bytes;
 }
@@ -755,6 +770,7 @@ extern "C" int srlu_k1_config(int64_t n, int64_t l1, int64_t pad1, int dtype, in
     const int es = es_of(dtype);
     k1s::Cfg f;
     SRLU_REQUIRE(info != nullptr, SRLU_ERR_ARG, "k1_config: null info");
+    if (es && srlu_k1t_info(n, l1, pad1, es, info) == SRLU_OK) return SRLU_OK;
     if (!es || !k1s::config(n, l1, pad1, es, &f)) {
         for (int i = 0; i < 8; ++i) info[i] = 0;
         return SRLU_ERR_UNSUPPORTED;
@@ -769,6 +785,9 @@ extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, in
                                 size_t sched_bytes, srlu_stream_t stream) {
     const int es = es_of(dtype);
     k1s::Cfg f;
+    if (es && srlu_k1t_plan_bytes(n, l1, pad1, es))
+        return srlu_k1t_plan(sorted1, bptr1, n, l1, pad1, es, sched, sched_bytes,
+                             (cudaStream_t)stream);
     SRLU_REQUIRE(es && k1s::config(n, l1, pad1, es, &f), SRLU_ERR_UNSUPPORTED,
                  "k1_schedule: shape not supported by the scheduled kernel");
     SRLU_REQUIRE(sched_bytes >= (size_t)f.ws_bytes, SRLU_ERR_WORKSPACE,
@@ -808,6 +827,12 @@ extern "C" int srlu_sketch_right_dense_sched(const void *a, int dtype, int64_t m
     SRLU_REQUIRE(m >= 1 && n >= 1 && lda >= n && l1 >= 1 && l1 <= n && k1 >= 1 && k1 <= pad1 &&
                      ldy >= k1,
                  SRLU_ERR_ARG, "sketch_right_dense_sched: bad sizes");
+    if (es && srlu_k1t_plan_bytes(n, l1, pad1, es)) {
+        SRLU_REQUIRE((uintptr_t)a % 16 == 0 && (lda * es) % 16 == 0, SRLU_ERR_UNSUPPORTED,
+                     "sketch_right_dense_sched: A must be 16-byte aligned with 16-byte row pitch");
+        return srlu_k1t_run(a, es, m, n, lda, sched, sched_bytes, l1, phase1, idx1, k1, pad1, mult1,
+                            y, ldy, nonfinite, (cudaStream_t)stream);
+    }
     SRLU_REQUIRE(es && k1s::config(n, l1, pad1, es, &f), SRLU_ERR_UNSUPPORTED,
                  "sketch_right_dense_sched: shape not supported by the scheduled kernel");
     SRLU_REQUIRE(sched_bytes >= (size_t)f.ws_bytes, SRLU_ERR_WORKSPACE,
