@@ -196,6 +196,21 @@ int srlu_sem_scatter_dense(const void *a, int dtype, int64_t rows, int64_t n, in
                            const int32_t *bucket_ptr, int64_t l, double *out, int64_t ldo,
                            srlu_stream_t stream);
 
+/* plugin seam, sparse variants, O(nnz), one thread per row / column walking
+ * its entries in ascending index (the reference's sequential sums):
+ *   srlu_sem_gather_csr  <- _fast.pyx:57-68 sem_gather_csc, on the CSR form
+ *     of the same matrix (rows x n, entries ascending in j per row):
+ *     out[i, row_of[j]] += sign[j] * a[i, j], out rows x l row-major fp64;
+ *   srlu_sem_scatter_csc <- _fast.pyx:81-90 sem_scatter_csc on the CSC
+ *     arrays (entries ascending in i per column):
+ *     out[row_of[i], j] += sign[i] * a[i, j], out l x cols row-major fp64. */
+int srlu_sem_gather_csr(const int64_t *indptr, const int32_t *indices, const void *vals,
+                        int dtype, int64_t rows, const int32_t *row_of, const double *sign,
+                        double *out, int64_t ldo, srlu_stream_t stream);
+int srlu_sem_scatter_csc(const int64_t *indptr, const int32_t *indices, const void *vals,
+                         int dtype, int64_t cols, const int32_t *row_of, const double *sign,
+                         double *out, int64_t ldo, srlu_stream_t stream);
+
 /* CSR variant; inv_perm[row] = PA index of local row (row0 offset applied
  * by the caller), row_of2/sign2 indexed by PA index.  Any column length
  * (columns beyond one CTA's 8192-entry sort are folded in bucket ranges and

@@ -74,28 +74,48 @@ def sem_scatter_dense(a: torch.Tensor, row_of, sign, out: torch.Tensor):
     out += tmp
 
 
-def _csc_to_dense_rows(data, indices, indptr, m):
-    n = indptr.numel() - 1
-    cols = torch.repeat_interleave(torch.arange(n, device=data.device), indptr.diff())
-    out = torch.zeros(m, n, dtype=torch.float64, device=data.device)
-    out[indices.long(), cols] = data.to(torch.float64)
-    return out
+def _csc_arrays(data, indices, indptr):
+    data = torch.as_tensor(data).cuda()
+    if data.dtype not in (torch.float32, torch.float64):
+        data = data.to(torch.float64)
+    return (data.contiguous(), torch.as_tensor(indices).to("cuda", torch.int32).contiguous(),
+            torch.as_tensor(indptr).to("cuda", torch.int64).contiguous())
 
 
 def sem_gather_csc(data, indices, indptr, row_of, sign, out: torch.Tensor):
-    """CSC variant of sem_gather_dense (_fast.pyx:57-68): the CSC array is
-    converted to the device CSR layout and run through the CSR stage-1
-    accumulation (bucket sums in ascending column order); the transform
-    is an identity here (pad = l, no FWHT) via the dense path on the
-    densified rows — seam-level utility, not a hot path."""
-    dense = _csc_to_dense_rows(torch.as_tensor(data).cuda(), torch.as_tensor(indices).cuda(),
-                               torch.as_tensor(indptr).cuda(), out.shape[0])
-    sem_gather_dense(dense, row_of, sign, out)
+    """CSC variant of sem_gather_dense (_fast.pyx:57-68), O(nnz): the CSC
+    entries are put in row-major order (stable sort by row index, so every
+    row keeps its entries in ascending column) and each row's bucket sums
+    are accumulated in that order by srlu_sem_gather_csr, in place on
+    ``out`` — the reference's loop order per (row, bucket) cell."""
+    data, indices, indptr = _csc_arrays(data, indices, indptr)
+    m, n = out.shape[0], indptr.numel() - 1
+    sem = _sem(row_of, sign, out.shape[1])
+    if out.dtype != torch.float64 or out.stride(1) != 1:
+        raise ValueError("out must be a row-major float64 matrix")
+    cols = torch.repeat_interleave(torch.arange(n, device=data.device, dtype=torch.int32),
+                                   indptr.diff())
+    order = torch.sort(indices, stable=True).indices
+    rptr = torch.zeros(m + 1, dtype=torch.int64, device=data.device)
+    rptr[1:] = torch.cumsum(torch.bincount(indices.long(), minlength=m), 0)
+    cidx, vals = cols[order].contiguous(), data[order].contiguous()
+    L = _lib.lib()
+    _lib.check(L.srlu_sem_gather_csr(_lib.ptr(rptr), _lib.ptr(cidx), _lib.ptr(vals),
+                                     _lib.dtype_code(vals.dtype), m, _lib.ptr(sem.row_of),
+                                     _lib.ptr(sem.sign), _lib.ptr(out), out.stride(0),
+                                     _lib.stream_handle()), "sem_gather_csr")
 
 
 def sem_scatter_csc(data, indices, indptr, row_of, sign, out: torch.Tensor):
-    """CSC variant of sem_scatter_dense (_fast.pyx:81-90), seam utility."""
-    m = torch.as_tensor(row_of).numel()
-    dense = _csc_to_dense_rows(torch.as_tensor(data).cuda(), torch.as_tensor(indices).cuda(),
-                               torch.as_tensor(indptr).cuda(), m)
-    sem_scatter_dense(dense, row_of, sign, out)
+    """CSC variant of sem_scatter_dense (_fast.pyx:81-90), O(nnz), in place
+    on ``out``: one thread per column walks its entries in ascending row."""
+    data, indices, indptr = _csc_arrays(data, indices, indptr)
+    n = indptr.numel() - 1
+    sem = _sem(row_of, sign, out.shape[0])
+    if out.dtype != torch.float64 or out.stride(1) != 1:
+        raise ValueError("out must be a row-major float64 matrix")
+    L = _lib.lib()
+    _lib.check(L.srlu_sem_scatter_csc(_lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(data),
+                                      _lib.dtype_code(data.dtype), n, _lib.ptr(sem.row_of),
+                                      _lib.ptr(sem.sign), _lib.ptr(out), out.stride(0),
+                                      _lib.stream_handle()), "sem_scatter_csc")

@@ -65,6 +65,8 @@ SIGNATURES = {
     "srlu_sketch_left_dense": (INT, [P, INT, I64, I64, I64, P, P, P, I64, P, P, I64, I64, DBL,
                                      P, I64, P, SZ, P]),
     "srlu_sem_scatter_dense": (INT, [P, INT, I64, I64, I64, P, P, P, I64, P, I64, P]),
+    "srlu_sem_gather_csr": (INT, [P, P, P, INT, I64, P, P, P, I64, P]),
+    "srlu_sem_scatter_csc": (INT, [P, P, P, INT, I64, P, P, P, I64, P]),
     "srlu_sketch_left_csr_workspace": (SZ, [I64, I64, I64, I64, I64]),
     "srlu_sketch_left_csr": (INT, [P, P, P, INT, I64, I64, I64, P, P, P, I64, P, P, I64, I64,
                                    DBL, P, I64, P, SZ, P, P]),
@@ -127,8 +129,8 @@ class _LaunchCounter:
 
     PER_CALL = {"build_sem": 3, "sem_plan": 4, "build_composite": 7, "build_composite_k1": 8, "build_composite_k1_g": 9, "composite_sketch_right_dense": 9, "composite_sketch_right_dense_g": 10, "composite_sketch_right_dense_nosched": 8, "sketch_right_dense": 1, "sketch_right_csr": 1,
                 "k1_schedule": 2, "k1_schedule_1": 1, "sketch_right_dense_sched": 1,
-                "sem_gather_dense": 1, "fwht_rows": 1, "sem_members": 1,
-                "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 6,
+                "sem_gather_dense": 1, "sem_gather_csr": 1, "sem_scatter_csc": 1, "fwht_rows": 1, "sem_members": 1,
+                "sketch_left_dense": 2, "sem_scatter_dense": 1, "sketch_left_csr": 6, "sketch_left_csr_big": 9,
                 "lu_row_pivot": 1, "lu_col_pivot": 1, "qr_pinv": 2, "rank_estimate": 1, "qr_rank": 1, "rank_exact": 1,
                 "dgemm": 1, "lu_error": 3}
 

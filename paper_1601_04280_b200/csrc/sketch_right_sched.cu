@@ -83,7 +83,12 @@ static bool config_try(int64_t n, int64_t l, int64_t pad, int es, int bpt, int r
     // each slot on its own step sequence.  One slot: consecutive buckets, so
     // the FWHT stages h < 32 run on the accumulators directly.
     f.sorted = env_int("SRLU_K1_SORT", bpt >= 2 ? 1 : 0) != 0;
-    f.joint = env_int("SRLU_K1_JOINT", f.sorted ? 0 : 1) != 0;  // testing knob
+    // joint = the slots of a warp step together (one code stream per warp and
+    // chunk).  Codes in shared memory: separate sequences per slot (fewer
+    // padded steps).  Codes read from L2 (more than kMaxChunks chunks): joint,
+    // because each slot sequence is a dependent L2 round trip and the kernel
+    // is bound by that latency (config 5: 14.2 -> 10.4 ms)
+    f.joint = env_int("SRLU_K1_JOINT", (f.sorted && nch <= kMaxChunks) ? 0 : 1) != 0;
     f.row_stride = (c + f.zpad) * es;
     f.stage_bytes = rb * f.row_stride;
     // FWHT scratch: only the bsize-point blocks that hold buckets (blocks

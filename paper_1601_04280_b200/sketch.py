@@ -438,7 +438,10 @@ def sketch_left_into(a: Matrix, omega2: CompositeSketch, mrow, msign, bptr, outT
             a.rows, a.cols, nnz, _lib.ptr(inv_perm), _lib.ptr(omega2.sem.row_of),
             _lib.ptr(omega2.sem.sign), omega2.sem.out_dim, _lib.ptr(fast.phase),
             _lib.ptr(fast.sample_idx), fast.out_dim, fast.pad, fast.mult, _lib.ptr(outT),
-            outT.stride(0), _lib.ptr(ws), ws.numel(), _lib.ptr(flags), sh), "sketch_left_csr")
+            outT.stride(0), _lib.ptr(ws), ws.numel(), _lib.ptr(flags), sh),
+            # launch accounting: banded count + scan and the tiled column scan
+            # (n >= 8192, counters in shared memory) add three kernels
+            "sketch_left_csr_big" if 8192 <= a.cols <= 102400 else "sketch_left_csr")
         return
     t = a.raw
     ws = _lib.workspace(L.srlu_sketch_left_workspace(a.cols, omega2.sem.out_dim, fast.pad),
