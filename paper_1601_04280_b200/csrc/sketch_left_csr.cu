@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(256) csr_scan_tsum_kernel(int64_t *__restrict_
 __global__ void __launch_bounds__(256) csr_scan_apply_kernel(const int *__restrict__ cnt,
                                                              int64_t n,
                                                              const int64_t *__restrict__ tsum,
-                                                             int64_t *__restrict__ colptr) {
+                                                             int64_t *__restrict__ colptr,
+                                                             int *__restrict__ cursor) {
     __shared__ int64_t wsum[8];
     const int64_t j0 = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
     int c[4];
@@ -160,7 +161,11 @@ __global__ void __launch_bounds__(256) csr_scan_apply_kernel(const int *__restri
     int64_t run = tsum[blockIdx.x] + block_excl_scan_256(s, &tot, wsum);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        if (j0 + u < n) colptr[j0 + u] = run;
+        if (j0 + u < n) {
+            colptr[j0 + u] = run;
+            // absolute fill cursor (nnz < 2^32): the fill kernel needs no colptr gather
+            if (cursor != nullptr) cursor[j0 + u] = (int)(unsigned)run;
+        }
         run += c[u];
     }
 }
@@ -213,6 +218,7 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
                                 const int32_t *__restrict__ row_of2,
                                 const double *__restrict__ sign2,
                                 const int64_t *__restrict__ colptr, int *__restrict__ fill,
+                                int abs_cursor,
                                 void *__restrict__ ent, const int *__restrict__ modep) {
     const int lane = threadIdx.x & 31;
     const int mode = sizeof(T) == 4 ? *modep : 0;
@@ -255,7 +261,9 @@ __global__ void csr_fill_kernel(const int64_t *__restrict__ indptr,
                 int64_t slot[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    slot[u] = j[u] >= 0 ? colptr[j[u]] + atomicAdd(fill + j[u], 1) : 0;
+                    slot[u] = j[u] < 0 ? 0
+                              : abs_cursor ? (int64_t)(unsigned)atomicAdd(fill + j[u], 1)
+                                           : colptr[j[u]] + atomicAdd(fill + j[u], 1);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     if (j[u] < 0) continue;
@@ -800,6 +808,8 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
     const size_t band_smem = (size_t)((n + 1) / 2) * 4;
     SRLU_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int) * n, s));
     SRLU_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int) * n, s));
+    // cursors start at the column's first slot (one scattered access per entry less)
+    const int abs_cursor = n >= 8 * kScanTile && nnz < (1LL << 32) - 1 ? 1 : 0;
     SRLU_CUDA(cudaMemsetAsync(w.mode, 0, sizeof(int) * 4, s));
     if (rows > 0) {
         int64_t blocks = ceil_div(rows, 256);
@@ -827,7 +837,8 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         SRLU_CUDA(cudaMemsetAsync(w.maxcnt, 0, sizeof(int), s));
         csr_scan_tiles_kernel<<<ntiles, 256, 0, s>>>(w.cnt, n, w.tsum, w.maxcnt);
         csr_scan_tsum_kernel<<<1, 256, 0, s>>>(w.tsum, ntiles, w.colptr + n);
-        csr_scan_apply_kernel<<<ntiles, 256, 0, s>>>(w.cnt, n, w.tsum, w.colptr);
+        csr_scan_apply_kernel<<<ntiles, 256, 0, s>>>(w.cnt, n, w.tsum, w.colptr,
+                                                     abs_cursor ? w.fill : nullptr);
         SRLU_CHECK_LAUNCH("csr_scan_apply_kernel");
     } else {
         csr_col_scan_kernel<<<1, 1024, 0, s>>>(w.cnt, n, w.colptr, w.maxcnt);
@@ -844,7 +855,7 @@ static int run_csr_left(const int64_t *indptr, const int32_t *indices, const T *
         int64_t blocks = ceil_div(rows * 32, 256);
         if (blocks > 148 * 16) blocks = 148 * 16;
         csr_fill_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(indptr, indices, vals, rows, inv_perm,
-                                                           row_of2, sign2, w.colptr, w.fill,
+                                                           row_of2, sign2, w.colptr, w.fill, abs_cursor,
                                                            w.ent, w.mode);
         SRLU_CHECK_LAUNCH("csr_fill_kernel");
     }
