@@ -80,7 +80,10 @@ struct Cfg {
 
 // Deterministic from (n, l, pad, es): the plan and the kernel agree.
 static bool config(int64_t n, int64_t l, int64_t pad, int es, Cfg *cf) {
-    if (env_int("SRLU_K1_TMEM", 1) == 0) return false;
+    // opt-in experiment (SRLU_K1_TMEM=1): bit-exact, but 0.49 ms at config 2
+    // against 0.247 ms for the scheduled kernel (issue-bound: ~19 instructions
+    // per 32-row gather step plus the skew pass; profiles/r02/k1t_*.txt)
+    if (env_int("SRLU_K1_TMEM", 0) == 0) return false;
     if (pad < 128 || pad > 1024 || l < 1 || l > pad || n < 1 || n > (1 << 23)) return false;
     if (es != 4 && es != 8) return false;
     Cfg f{};
