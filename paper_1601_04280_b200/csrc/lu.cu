@@ -139,7 +139,169 @@ __device__ inline void block_best(unsigned long long &abs, unsigned &pos, int &e
 // the panel lives in an attribute-major workspace [GB][M] (64 MB at M = 1M:
 // L2-resident, every column access coalesced across threads), with GB-wide
 // register rows and several entities' loads in flight per thread.
-template <int MODE, int GB = 0>
+// Two-level trailing update (lu_outer_width): the nb2 = x_hi - Jo pivots of the
+// outer block [Jo, x_hi) applied to the columns [x_hi, k) of this CTA's live
+// rows.  Kept out of line so that its registers do not weigh on the kernel's
+// per-step loops.
+template <int MODE>
+__device__ __noinline__ void lu_outer_update(const LuParams &p, double *PRo, double *Acho,
+                                             const double *PR, const int *pwo, const int *pos,
+                                             int J, int Jo, int x_hi, int ne, int64_t e0,
+                                             double thresh) {
+    const int tid = threadIdx.x;
+    const int k = p.k, b = p.b;
+        const int nb2 = x_hi - Jo;   // pivots of the outer block
+        const int jl = J - Jo;       // first one of the last inner panel
+        // PRo(ls, l2 <= ls): pivot row ls's panel values at the earlier
+        // pivots' columns (ROW: its multipliers; COL: its own values, the
+        // pivot on the diagonal).  The last inner panel's are still in PR
+        // (its write-back may not be visible to other CTAs yet); the others
+        // were written back before at least one grid barrier.
+        for (int w = tid; w < nb2 * nb2; w += blockDim.x) {
+            const int ls = w / nb2, l2 = w - ls * nb2;
+            if (l2 > ls) continue;
+            PRo[ls * kLuB2Max + l2] =
+                (ls >= jl && l2 >= jl) ? PR[(ls - jl) * b + (l2 - jl)]
+                                       : __ldcg(p.w + (int64_t)pwo[ls] * p.ld + Jo + l2);
+        }
+        __syncthreads();
+        for (int x0 = x_hi; x0 < k; x0 += kLuXC) {
+            const int xc = min(kLuXC, k - x0);
+            for (int w = tid; w < nb2 * xc; w += blockDim.x) {
+                const int ls = w / xc, c = w - ls * xc;
+                Acho[ls * kLuXC + c] = __ldcg(p.w + (int64_t)pwo[ls] * p.ld + x0 + c);
+            }
+            __syncthreads();
+            {   // the pivot rows' values: the same blocked recurrence over nb2 pivots
+                constexpr int KB = 8;
+                const int c = tid % kLuXC, g = tid / kLuXC;
+                for (int s0 = 0; s0 < nb2; s0 += KB) {
+                    const int ls = s0 + g;
+                    if (s0 > 0 && g < KB && ls < nb2 && c < xc) {
+                        double v = Acho[ls * kLuXC + c];
+                        const double *pr = PRo + ls * kLuB2Max;
+                        for (int l2 = 0; l2 < s0; ++l2)
+                            v = MODE == MODE_ROW
+                                    ? __dsub_rn(v, __dmul_rn(pr[l2], Acho[l2 * kLuXC + c]))
+                                    : __dsub_rn(v, __dmul_rn(Acho[l2 * kLuXC + c], pr[l2]));
+                        Acho[ls * kLuXC + c] = v;
+                    }
+                    __syncthreads();
+                    if (g == 0 && c < xc) {
+                        const int nb = min(KB, nb2 - s0);
+                        double a[KB];
+#pragma unroll
+                        for (int i = 0; i < KB; ++i)
+                            a[i] = i < nb ? Acho[(s0 + i) * kLuXC + c] : 0.0;
+#pragma unroll
+                        for (int i = 0; i < KB; ++i) {
+                            if (i < nb) {
+                                double v = a[i];
+                                const double *pr = PRo + (s0 + i) * kLuB2Max + s0;
+#pragma unroll
+                                for (int j = 0; j < i; ++j)
+                                    v = MODE == MODE_ROW ? __dsub_rn(v, __dmul_rn(pr[j], a[j]))
+                                                         : __dsub_rn(v, __dmul_rn(a[j], pr[j]));
+                                if (MODE != MODE_ROW) {
+                                    const double pv = pr[i];
+                                    v = fabs(pv) > thresh ? v / pv : 0.0;
+                                }
+                                a[i] = v;
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < KB; ++i) {
+                            if (i < nb) {
+                                Acho[(s0 + i) * kLuXC + c] = a[i];
+                                if (blockIdx.x == 0)
+                                    p.piv[(int64_t)(Jo + s0 + i) * k + x0 + c] = a[i];
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            
+            {   // rows: RPW per warp pass, the row's nb2 multipliers (its
+                // columns [Jo, x_hi), one coalesced load) held across the
+                // lanes and broadcast by shuffles
+                constexpr int RPW = kLuRPW;
+                const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+                const bool c0ok = lane < xc, c1ok = lane + 32 < xc;
+                const int a1i = lane + 32 < kLuXC ? lane + 32 : lane;
+                const int stride = nwarp * RPW;
+                double vn[RPW][2], pmn[RPW];
+                bool ln[RPW];
+                auto fetch = [&](int eb) {
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r) {
+                        const int e = eb + r;
+                        ln[r] = e < ne && pos[e] >= x_hi;  // this block's pivots are frozen
+                        const double *gr = p.w + (e0 + e) * p.ld;
+                        vn[r][0] = ln[r] && c0ok ? gr[x0 + lane] : 0.0;
+                        vn[r][1] = ln[r] && c1ok ? gr[x0 + lane + 32] : 0.0;
+                        pmn[r] = ln[r] && lane < nb2 ? gr[Jo + lane] : 0.0;
+                    }
+                };
+                const int l2pf = p.l2pf;
+                auto prefetch = [&](int ebp) {
+                    if (lane < RPW) {
+                        const int e = ebp + lane;
+                        if (e < ne && pos[e] >= x_hi) {
+                            const uintptr_t a0 = (uintptr_t)(p.w + (e0 + e) * p.ld + x0);
+                            const uintptr_t lo = a0 & ~(uintptr_t)15;
+                            const uintptr_t hi = (a0 + (uintptr_t)xc * 8 + 15) & ~(uintptr_t)15;
+                            bulk_prefetch_l2((const void *)lo, (unsigned)(hi - lo));
+                        }
+                    }
+                };
+                int eb = warp * RPW;
+                if (l2pf > 0)
+                    for (int d = 1; d <= l2pf; ++d) prefetch(eb + d * stride);
+                if (eb < ne) fetch(eb);
+                for (; eb < ne; eb += stride) {
+                    if (l2pf > 0) prefetch(eb + (l2pf + 1) * stride);
+                    double v[RPW][2], pm[RPW];
+                    bool live[RPW];
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r) {
+                        v[r][0] = vn[r][0];
+                        v[r][1] = vn[r][1];
+                        live[r] = ln[r];
+                        pm[r] = pmn[r];
+                    }
+                    if (eb + stride < ne) fetch(eb + stride);
+                    for (int ls = 0; ls < nb2; ++ls) {
+                        const double a0 = Acho[ls * kLuXC + lane];
+                        const double a1 = Acho[ls * kLuXC + a1i];
+#pragma unroll
+                        for (int r = 0; r < RPW; ++r) {
+                            const double pv = __shfl_sync(0xffffffffu, pm[r], ls);
+                            if (MODE == MODE_ROW) {
+                                v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
+                                v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
+                            } else {
+                                v[r][0] = __dsub_rn(v[r][0], __dmul_rn(a0, pv));
+                                v[r][1] = __dsub_rn(v[r][1], __dmul_rn(a1, pv));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < RPW; ++r) {
+                        if (!live[r]) continue;
+                        double *gp = p.w + (e0 + eb + r) * p.ld + x0 + lane;
+                        if (c0ok) gp[0] = v[r][0];
+                        if (c1ok) gp[32] = v[r][1];
+                    }
+                }
+            }
+            __syncthreads();
+            
+        }
+
+}
+
+template <int MODE, int GB = 0, bool TWO = false>
 __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_abs[32];
@@ -161,7 +323,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     double *PR = spanel + (GB ? 0 : (size_t)rpc * bs);              // b x b
     double *u = PR + (size_t)b * b;                                 // b
     double *Ach = u + b;                                            // b x kLuXC
-    const int b2 = p.b2;
+    const int b2 = TWO ? p.b2 : 0;
     double *PRo = Ach + (size_t)b * kLuXC;                          // b2 x kLuB2Max
     double *Acho = PRo + (size_t)b2 * kLuB2Max;                     // b2 x kLuXC
     int *pos = reinterpret_cast<int *>(Acho + (size_t)b2 * kLuXC);  // rpc
@@ -639,156 +801,10 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
             LU_T(5);  // trace: the rows' trailing update of this chunk
         }
 
-        // ---- outer block complete: its nb2 pivots applied to the columns [x_hi, k)
-        if (b2 && J + bw >= x_hi && x_hi < k) {
-            const int nb2 = x_hi - Jo;   // pivots of the outer block
-            const int jl = J - Jo;       // first one of the last inner panel
-            // PRo(ls, l2 <= ls): pivot row ls's panel values at the earlier
-            // pivots' columns (ROW: its multipliers; COL: its own values, the
-            // pivot on the diagonal).  The last inner panel's are still in PR
-            // (its write-back may not be visible to other CTAs yet); the others
-            // were written back before at least one grid barrier.
-            for (int w = tid; w < nb2 * nb2; w += blockDim.x) {
-                const int ls = w / nb2, l2 = w - ls * nb2;
-                if (l2 > ls) continue;
-                PRo[ls * kLuB2Max + l2] =
-                    (ls >= jl && l2 >= jl) ? PR[(ls - jl) * b + (l2 - jl)]
-                                           : __ldcg(p.w + (int64_t)pwo[ls] * p.ld + Jo + l2);
-            }
-            __syncthreads();
-            for (int x0 = x_hi; x0 < k; x0 += kLuXC) {
-                const int xc = min(kLuXC, k - x0);
-                for (int w = tid; w < nb2 * xc; w += blockDim.x) {
-                    const int ls = w / xc, c = w - ls * xc;
-                    Acho[ls * kLuXC + c] = __ldcg(p.w + (int64_t)pwo[ls] * p.ld + x0 + c);
-                }
-                __syncthreads();
-                {   // the pivot rows' values: the same blocked recurrence over nb2 pivots
-                    constexpr int KB = 8;
-                    const int c = tid % kLuXC, g = tid / kLuXC;
-                    for (int s0 = 0; s0 < nb2; s0 += KB) {
-                        const int ls = s0 + g;
-                        if (s0 > 0 && g < KB && ls < nb2 && c < xc) {
-                            double v = Acho[ls * kLuXC + c];
-                            const double *pr = PRo + ls * kLuB2Max;
-                            for (int l2 = 0; l2 < s0; ++l2)
-                                v = MODE == MODE_ROW
-                                        ? __dsub_rn(v, __dmul_rn(pr[l2], Acho[l2 * kLuXC + c]))
-                                        : __dsub_rn(v, __dmul_rn(Acho[l2 * kLuXC + c], pr[l2]));
-                            Acho[ls * kLuXC + c] = v;
-                        }
-                        __syncthreads();
-                        if (g == 0 && c < xc) {
-                            const int nb = min(KB, nb2 - s0);
-                            double a[KB];
-#pragma unroll
-                            for (int i = 0; i < KB; ++i)
-                                a[i] = i < nb ? Acho[(s0 + i) * kLuXC + c] : 0.0;
-#pragma unroll
-                            for (int i = 0; i < KB; ++i) {
-                                if (i < nb) {
-                                    double v = a[i];
-                                    const double *pr = PRo + (s0 + i) * kLuB2Max + s0;
-#pragma unroll
-                                    for (int j = 0; j < i; ++j)
-                                        v = MODE == MODE_ROW ? __dsub_rn(v, __dmul_rn(pr[j], a[j]))
-                                                             : __dsub_rn(v, __dmul_rn(a[j], pr[j]));
-                                    if (MODE != MODE_ROW) {
-                                        const double pv = pr[i];
-                                        v = fabs(pv) > thresh ? v / pv : 0.0;
-                                    }
-                                    a[i] = v;
-                                }
-                            }
-#pragma unroll
-                            for (int i = 0; i < KB; ++i) {
-                                if (i < nb) {
-                                    Acho[(s0 + i) * kLuXC + c] = a[i];
-                                    if (blockIdx.x == 0)
-                                        p.piv[(int64_t)(Jo + s0 + i) * k + x0 + c] = a[i];
-                                }
-                            }
-                        }
-                        __syncthreads();
-                    }
-                }
-                LU_T(4);
-                {   // rows: RPW per warp pass, the row's nb2 multipliers (its
-                    // columns [Jo, x_hi), one coalesced load) held across the
-                    // lanes and broadcast by shuffles
-                    constexpr int RPW = kLuRPW;
-                    const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-                    const bool c0ok = lane < xc, c1ok = lane + 32 < xc;
-                    const int a1i = lane + 32 < kLuXC ? lane + 32 : lane;
-                    const int stride = nwarp * RPW;
-                    double vn[RPW][2], pmn[RPW];
-                    bool ln[RPW];
-                    auto fetch = [&](int eb) {
-#pragma unroll
-                        for (int r = 0; r < RPW; ++r) {
-                            const int e = eb + r;
-                            ln[r] = e < ne && pos[e] >= x_hi;  // this block's pivots are frozen
-                            const double *gr = p.w + (e0 + e) * p.ld;
-                            vn[r][0] = ln[r] && c0ok ? gr[x0 + lane] : 0.0;
-                            vn[r][1] = ln[r] && c1ok ? gr[x0 + lane + 32] : 0.0;
-                            pmn[r] = ln[r] && lane < nb2 ? gr[Jo + lane] : 0.0;
-                        }
-                    };
-                    const int l2pf = p.l2pf;
-                    auto prefetch = [&](int ebp) {
-                        if (lane < RPW) {
-                            const int e = ebp + lane;
-                            if (e < ne && pos[e] >= x_hi) {
-                                const uintptr_t a0 = (uintptr_t)(p.w + (e0 + e) * p.ld + x0);
-                                const uintptr_t lo = a0 & ~(uintptr_t)15;
-                                const uintptr_t hi = (a0 + (uintptr_t)xc * 8 + 15) & ~(uintptr_t)15;
-                                bulk_prefetch_l2((const void *)lo, (unsigned)(hi - lo));
-                            }
-                        }
-                    };
-                    int eb = warp * RPW;
-                    if (l2pf > 0)
-                        for (int d = 1; d <= l2pf; ++d) prefetch(eb + d * stride);
-                    if (eb < ne) fetch(eb);
-                    for (; eb < ne; eb += stride) {
-                        if (l2pf > 0) prefetch(eb + (l2pf + 1) * stride);
-                        double v[RPW][2], pm[RPW];
-                        bool live[RPW];
-#pragma unroll
-                        for (int r = 0; r < RPW; ++r) {
-                            v[r][0] = vn[r][0];
-                            v[r][1] = vn[r][1];
-                            live[r] = ln[r];
-                            pm[r] = pmn[r];
-                        }
-                        if (eb + stride < ne) fetch(eb + stride);
-                        for (int ls = 0; ls < nb2; ++ls) {
-                            const double a0 = Acho[ls * kLuXC + lane];
-                            const double a1 = Acho[ls * kLuXC + a1i];
-#pragma unroll
-                            for (int r = 0; r < RPW; ++r) {
-                                const double pv = __shfl_sync(0xffffffffu, pm[r], ls);
-                                if (MODE == MODE_ROW) {
-                                    v[r][0] = __dsub_rn(v[r][0], __dmul_rn(pv, a0));
-                                    v[r][1] = __dsub_rn(v[r][1], __dmul_rn(pv, a1));
-                                } else {
-                                    v[r][0] = __dsub_rn(v[r][0], __dmul_rn(a0, pv));
-                                    v[r][1] = __dsub_rn(v[r][1], __dmul_rn(a1, pv));
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int r = 0; r < RPW; ++r) {
-                            if (!live[r]) continue;
-                            double *gp = p.w + (e0 + eb + r) * p.ld + x0 + lane;
-                            if (c0ok) gp[0] = v[r][0];
-                            if (c1ok) gp[32] = v[r][1];
-                        }
-                    }
-                }
-                __syncthreads();
-                LU_T(5);
-            }
+        // ---- outer block complete: its pivots applied to the columns [x_hi, k)
+        if (TWO && b2 && J + bw >= x_hi && x_hi < k) {
+            lu_outer_update<MODE>(p, PRo, Acho, PR, pwo, pos, J, Jo, x_hi, ne, e0, thresh);
+            LU_T(5);
         }
     }
 
@@ -2318,16 +2334,17 @@ static size_t lu_base_workspace(int64_t k) {
 static inline int64_t lu_gpanel_ld(int64_t M) { return (M + 31) & ~(int64_t)31; }
 
 // Outer block of the two-level trailing update for panels of width b (0 =
-// one level).  Measured (tools/lu_time.py, tools/lu_b2_trace.sh): it cuts the
-// HBM traffic of the trailing updates by b2 / b, which pays where they are
-// traffic-bound — the L2-panel variant on very tall inputs (config 4 shape,
-// 1048576 x 120: 10.56 -> 10.0 ms) — but not for the shared-memory panel
-// (config 3 shape, 262144 x 220: 4.16 -> 4.52 ms): there the update is bound
-// by its instruction stream at 16 warps per SM, the narrow in-block chunks
-// leave lanes idle and the extra 24 KB of shared memory narrow the panel.
-// Default: on for the L2 panel only; SRLU_LU_B2 = 0 / 1 forces it off / on.
+// one level).  Opt-in experiment (SRLU_LU_B2=1), bit-exact (tests), measured
+// slower on B200 and therefore off: it cuts the HBM traffic of the trailing
+// updates by b2 / b, but those are bound by their instruction stream at 16
+// warps per SM, not by traffic — config 3 shape (262144 x 220, shared-memory
+// panel) 4.16 -> 4.52 ms (narrow in-block chunks leave lanes idle, the extra
+// 24 KB of shared memory narrow the panel); config 4 (1048576 x 120, L2
+// panel) LU(Y) 8.74 -> 10.4 ms (the out-of-line update spills at the
+// 128-register cap).  The kernels without it (TWO = false) are unchanged.
 static int lu_outer_width(int b, int64_t k, bool gpanel) {
-    bool on = gpanel;
+    (void)gpanel;
+    bool on = false;
     if (const char *env = getenv("SRLU_LU_B2")) on = atoi(env) != 0;  // testing knob
     if (!on || b >= k || 2 * b > kLuB2Max) return 0;
     return (kLuB2Max / b) * b;
@@ -2614,7 +2631,8 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     size_t smem = lu_smem_bytes(rpc, b, bs, prm.b2);
     SRLU_REQUIRE(smem <= budget, SRLU_ERR_UNSUPPORTED,
                  "lu: %lld entities per CTA do not fit in shared memory", (long long)rpc);
-    auto kern = gpanel ? lu_kernel<MODE, 8> : lu_kernel<MODE, 0>;
+    auto kern = gpanel ? (prm.b2 ? lu_kernel<MODE, 8, true> : lu_kernel<MODE, 8, false>)
+                       : (prm.b2 ? lu_kernel<MODE, 0, true> : lu_kernel<MODE, 0, false>);
     SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     SRLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLuThreads, smem));

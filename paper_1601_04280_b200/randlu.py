@@ -294,6 +294,21 @@ def _pinned_copy(t: torch.Tensor) -> torch.Tensor:
     return out
 
 
+_NVTX = bool(os.environ.get("SRLU_NVTX"))
+
+
+def _stage_mark(ev, i, stream):
+    """Stage boundary i: the CUDA event behind ``elapsed`` and, with
+    SRLU_NVTX=1, an NVTX range per stage (srlu.sketch1, srlu.lu1, ...) for
+    timeline profilers."""
+    ev[i].record(stream)
+    if _NVTX:
+        if i > 0:
+            torch.cuda.nvtx.range_pop()
+        if i < len(STAGES):
+            torch.cuda.nvtx.range_push("srlu." + STAGES[i])
+
+
 def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandLuResult:
     """One pass of Algorithm 1 (randlu.py:246-276).  Two streams: the side
     stream draws Omega2 and builds its plan while K1/K2 run, and runs the
@@ -305,7 +320,7 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev)
     ev = _stage_events(dev, len(STAGES) + 1)
-    ev[0].record(main)
+    _stage_mark(ev, 0, main)
 
     y = torch.empty(m, k1, dtype=torch.float64, device=dev)
     if a.is_sparse:
@@ -315,7 +330,7 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     else:  # draws, plan, schedule and K1 in one C call
         flag = torch.empty(1, dtype=torch.int32, device=dev)
         om1 = composite_sketch_right(a, k1, params.l1, kind, params.seed + 2 * attempt, y, flag)
-    ev[1].record(main)
+    _stage_mark(ev, 1, main)
 
     def omega2():
         # Omega2 (draws + plan + member table of L1) on the side stream,
@@ -336,7 +351,7 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
         om2, (mrow_l, msign_l, bptr2), ev_om2 = omega2()
     y_keep = y.clone() if keep else None
     perm, l1, _ = lu_row_pivot_dev(y)
-    ev[2].record(main)
+    _stage_mark(ev, 2, main)
     if small:
         om2, (mrow_l, msign_l, bptr2), ev_om2 = omega2()
 
@@ -366,18 +381,18 @@ def _attempt(a: Matrix, params: RandLuParams, attempt: int, keep: bool) -> RandL
     else:
         mrow, msign, _ = members(om2, perm, 0, m)
         sketch_left_into(a, om2, mrow, msign, bptr2, red_aT)
-    ev[3].record(main)
+    _stage_mark(ev, 3, main)
 
     main.wait_event(ev_pinv)
     core_t = dgemm(red_aT, pinv_t)      # (Omega2 P A)^T pinv^T = core^T, n x k1
-    ev[4].record(main)
+    _stage_mark(ev, 4, main)
     core_keep = core_t.clone() if keep else None
 
     # one SM left to the side stream's rank test (a cooperative launch would
     # otherwise wait for it)
     q, lt, ut = lu_col_pivot_dev(core_t, reserve_sms=1)
     l_final = dgemm(l1, lt, b_lower=True)
-    ev[5].record(main)
+    _stage_mark(ev, 5, main)
 
     # the one host sync of the attempt: rank test, non-finite flag, P, Q
     main.wait_stream(side)

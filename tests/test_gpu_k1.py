@@ -107,3 +107,30 @@ def test_unscheduled_k1_bit_exact(P, m, n, dt, l, k, monkeypatch):
     y = P.apply_sketch_right(P.Matrix.from_device(torch.from_numpy(a).cuda()), om)
     ref = O.apply_sketch_right(a.astype(np.float64), D.build_composite(k, l, n, seed))
     np.testing.assert_array_equal(y.numpy(), ref)
+
+
+# TMEM-accumulator kernel (csrc/sketch_right_tmem.cu), opt-in: lanes = rows,
+# bucket sums in tensor memory, 128 <= pad1 <= 1024
+K1T_SHAPES = [
+    (300, 2048, np.float64, 480, 60, "8"),     # one row group, fp64
+    (200, 4096, np.float32, 880, 110, "28"),   # three 8-row boxes + a 4-row tail box, skew warps
+    (4000, 4096, np.float32, 880, 110, "16"),  # several row blocks per CTA
+    (100, 3000, np.float64, 700, 64, "32"),    # fp64, four row groups
+    (257, 1024, np.float32, 200, 30, ""),      # pad 256 (64 slots per quarter), rows picked
+]
+
+
+@pytest.mark.parametrize("m,n,dt,l,k,rows", K1T_SHAPES)
+def test_tmem_k1_bit_exact(P, m, n, dt, l, k, rows, monkeypatch):
+    import torch
+    from oracle import draws as D
+    from oracle import randlu as O
+    monkeypatch.setenv("SRLU_K1_TMEM", "1")
+    if rows:
+        monkeypatch.setenv("SRLU_K1T_ROWS", rows)
+    seed = 23 + m
+    a = _wide_range(m, n, seed, dt)
+    om = P.build_composite(k, l, n, "hadamard", seed)
+    y = P.apply_sketch_right(P.Matrix.from_device(torch.from_numpy(a).cuda()), om)
+    ref = O.apply_sketch_right(a.astype(np.float64), D.build_composite(k, l, n, seed))
+    np.testing.assert_array_equal(y.numpy(), ref)

@@ -425,3 +425,70 @@ def test_stage1_unaligned_rows_fused_call(P, n, dt):
     ref = O.sparse_randomized_lu(a.astype(np.float64), prm, keep=True)
     np.testing.assert_array_equal(res.extras["Y"].cpu().numpy(), ref["Y"])
     np.testing.assert_array_equal(res.P.indices, ref["P"])
+
+
+# --------------------------------------------------------------------------
+# round-2 code paths behind knobs: every variant must stay bit-exact
+
+
+@pytest.mark.parametrize("mode", ["row", "col"])
+@pytest.mark.parametrize("gpanel", ["0", "1"])
+def test_lu_two_level_trailing_update_bit_exact(P, mode, gpanel, monkeypatch):
+    """Grid LU with the opt-in outer-block (two-level) trailing update, for
+    the shared-memory panel and the L2 panel: same P/Q, L, U bits."""
+    monkeypatch.setenv("SRLU_LU_B2", "1")
+    monkeypatch.setenv("SRLU_LU_NO_HYBRID", "1")
+    monkeypatch.setenv("SRLU_LU_GPANEL", gpanel)
+    monkeypatch.setenv("SRLU_LU_MAX_GRID", "8")   # many rows per CTA: narrow panels, b2 = 4 b
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(77))
+    if mode == "row":
+        b = g.standard_normal((30000, 150))
+        b[:, 40:44] = b[:, :4] @ g.standard_normal((4, 4))   # dependent columns: threshold path
+        perm, lo, up = O.lu_row_pivot(b)
+        r = P.lu_row_pivot(b)
+        np.testing.assert_array_equal(r.P.indices, perm)
+        np.testing.assert_array_equal(r.L.numpy(), lo)
+        np.testing.assert_array_equal(r.U.numpy(), up)
+    else:
+        c = g.standard_normal((120, 25000))
+        q, lo, up = O.lu_col_pivot(c)
+        r = P.lu_col_pivot(c)
+        np.testing.assert_array_equal(r.Q.indices, q)
+        np.testing.assert_array_equal(r.L.numpy(), lo)
+        np.testing.assert_array_equal(r.U.numpy(), up)
+
+
+def test_lu_hybrid_without_cooperative_launch_bit_exact(P, monkeypatch):
+    """The hybrid LU launched without the cooperative attribute (what runs
+    under ncu): own grid barrier, same result."""
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(78))
+    b = g.standard_normal((9000, 96))
+    perm, lo, up = O.lu_row_pivot(b)
+    monkeypatch.setenv("SRLU_LU_NOCOOP", "1")
+    r = P.lu_row_pivot(b)
+    np.testing.assert_array_equal(r.P.indices, perm)
+    np.testing.assert_array_equal(r.L.numpy(), lo)
+    np.testing.assert_array_equal(r.U.numpy(), up)
+
+
+@pytest.mark.parametrize("knob", [None, ("SRLU_CSR_BANDS", "0"), ("SRLU_CSR_BANDFILL", "1")])
+def test_csr_wide_matrix_bit_exact(P, knob, monkeypatch):
+    """n >= 8192 columns: banded shared-memory column count, tiled column scan
+    and absolute fill cursors (default); the global-atomic count and the
+    banded fill behind their knobs."""
+    if knob:
+        monkeypatch.setenv(*knob)
+    from scipy.sparse import random as sprandom
+    from oracle import randlu as O
+    g = np.random.Generator(np.random.Philox(79))
+    m, n = 5000, 9000
+    a = sprandom(m, n, density=0.004, format="csr", random_state=g, dtype=np.float64)
+    a.data = g.standard_normal(a.nnz)
+    prm = dict(r=8, k1=16, l1=64, k2=24, l2=96, seed=3)
+    res = P.sparse_randomized_lu(P.Matrix.sparse(a), P.RandLuParams(**prm), keep=True)
+    ref = O.sparse_randomized_lu(a, prm, keep=True)
+    np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
+    np.testing.assert_array_equal(res.P.indices, ref["P"])
+    np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
