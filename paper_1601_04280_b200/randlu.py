@@ -165,9 +165,11 @@ def gaussian_randomized_lu(a, params: RandLuParams, keep: bool = False) -> RandL
     """randlu.py:216-219: the same pipeline with dense Gaussian projections
     G1 (k1 x n) and G2 (k2 x m) applied by plain FP64 matrix products
     (randlu.py:184-205) — the paper's comparison baseline.  The draws are
-    numpy's Philox(seed) standard normals (host, then uploaded); the products
-    run on cuBLAS DGEMM (cuSPARSE SpMM for CSR); the LUs, pseudo-inverse and
-    rank test are the same kernels as the sparse path."""
+    numpy's Philox(seed) standard normals (host, then uploaded: the ziggurat
+    stream is kept bit-identical to the reference's); for dense A the three
+    products run on the package's own FP64 tensor-core GEMM (srlu_dgemm, DMMA),
+    for CSR A on cuSPARSE SpMM; the LUs, pseudo-inverse and rank test are the
+    same kernels as the sparse path."""
     a = a if isinstance(a, Matrix) else Matrix(a)
     return _pipeline(a, params, keep, gaussian=True)
 
@@ -196,16 +198,21 @@ def _attempt_gaussian(a: Matrix, params: RandLuParams, attempt: int, keep: bool)
         a_op = a.raw.double() if a.raw.dtype != torch.float64 else a.raw
     if not bool(torch.isfinite(a_op.values() if a.is_sparse else a_op).all()):
         raise ValueError("matrix entries must be finite")
-    y = (a_op @ g1.t()).contiguous()                      # A . G1^T, m x k1
+    if a.is_sparse:
+        y = (a_op @ g1.t()).contiguous()                  # A . G1^T, m x k1 (SpMM)
+    else:
+        y = dgemm(a_op, g1.t().contiguous())
     ev[1].record(main)
     y_keep = y.clone() if keep else None
     perm, l1, _ = lu_row_pivot_dev(y)
     ev[2].record(main)
-    red_lT = (l1.t() @ g2.t()).contiguous()               # (G2 . L1)^T, k1 x k2
+    red_lT = dgemm(l1.t().contiguous(), g2.t().contiguous())   # (G2 . L1)^T, k1 x k2
     g2p = torch.empty_like(g2)
     g2p[:, perm] = g2                                      # G2 . (P A) = G2p . A
-    red_aT = (a_op.t() @ g2p.t()).contiguous() if a.is_sparse else \
-        (a_op.t() @ g2p.t()).contiguous()                  # (G2 P A)^T, n x k2
+    if a.is_sparse:
+        red_aT = (a_op.t() @ g2p.t()).contiguous()        # (G2 P A)^T, n x k2 (SpMM)
+    else:
+        red_aT = dgemm(a_op.t().contiguous(), g2p.t().contiguous())
     ev[3].record(main)
     pinv_t, rank = pinv_dev(red_lT)
     core_t = dgemm(red_aT, pinv_t)

@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
+import threading
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -292,7 +294,64 @@ def composite_sketch_right(a: Matrix, k, l, kind, seed, y: torch.Tensor, nonfini
                       (t, k1_dtype, y, nonfinite))
 
 
+# Sketch cache.  A composite sketch depends only on
+# (k, l, n, kind, seed) — not on A — so repeated decompositions with the same
+# parameters can reuse the draws, the bucket plan and the K1 schedule.  OFF by
+# default: the reference redraws on every call (randlu.py:250-251) and
+# bench.py times that work; enable with set_sketch_cache(True) or
+# SRLU_SKETCH_CACHE=1.  Entries hold device buffers (LRU, 8 by default).
+_CACHE = {"on": bool(os.environ.get("SRLU_SKETCH_CACHE")), "max": 8, "lock": threading.Lock(),
+          "map": {}, "hits": 0, "misses": 0}
+
+
+def set_sketch_cache(enabled: bool, max_entries: int = 8) -> None:
+    """Turn the composite-sketch cache on or off (off drops the entries)."""
+    with _CACHE["lock"]:
+        _CACHE["on"] = bool(enabled)
+        _CACHE["max"] = max(1, int(max_entries))
+        if not enabled:
+            _CACHE["map"].clear()
+
+
+def sketch_cache_stats() -> dict:
+    with _CACHE["lock"]:
+        return {"enabled": _CACHE["on"], "entries": len(_CACHE["map"]), "hits": _CACHE["hits"],
+                "misses": _CACHE["misses"]}
+
+
 def _composite(k, l, n, kind, seed, device, stream, k1_dtype, right):
+    if not _CACHE["on"]:
+        return _composite_build(k, l, n, kind, seed, device, stream, k1_dtype, right)
+    dev = torch.device(device) if device is not None else _default_device()
+    key = (int(k), int(l), int(n), kind, int(seed), dev.index if dev.index is not None else
+           torch.cuda.current_device(), k1_dtype)
+    with _CACHE["lock"]:
+        hit = _CACHE["map"].pop(key, None)
+        if hit is not None:
+            _CACHE["map"][key] = hit          # most recently used last
+            _CACHE["hits"] += 1
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    if hit is not None:
+        om, ev = hit
+        s.wait_event(ev)                      # the draws were enqueued on another stream
+        if right is not None:                 # the fused call's K1, on the cached sketch
+            t, _, y, nonfinite = right
+            with torch.cuda.stream(s):
+                nonfinite.zero_()
+            sketch_right_into(Matrix.from_device(t), om, y, nonfinite, stream=stream)
+        return om
+    om = _composite_build(k, l, n, kind, seed, device, stream, k1_dtype, right)
+    ev = torch.cuda.Event()
+    ev.record(s)
+    with _CACHE["lock"]:
+        _CACHE["misses"] += 1
+        _CACHE["map"][key] = (om, ev)
+        while len(_CACHE["map"]) > _CACHE["max"]:
+            _CACHE["map"].pop(next(iter(_CACHE["map"])))
+    return om
+
+
+def _composite_build(k, l, n, kind, seed, device, stream, k1_dtype, right):
     if kind not in (FOURIER, HADAMARD):
         raise ParameterError(f"unknown transform kind {kind!r}")
     if kind == FOURIER:

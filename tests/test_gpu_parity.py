@@ -492,3 +492,31 @@ def test_csr_wide_matrix_bit_exact(P, knob, monkeypatch):
     np.testing.assert_array_equal(_np(res.extras["Y"]), ref["Y"])
     np.testing.assert_array_equal(res.P.indices, ref["P"])
     np.testing.assert_array_equal(_np(res.extras["red_a"]), ref["red_a"])
+
+
+def test_sketch_cache_reuses_draws_bit_exact(P):
+    """Opt-in sketch cache: the second decomposition with the
+    same parameters reuses the draws / plan / K1 schedule and returns the
+    same bits; a different seed misses."""
+    import torch
+    g = np.random.Generator(np.random.Philox(5))
+    a = torch.from_numpy(g.standard_normal((900, 700))).cuda()
+    prm = dict(r=10, k1=18, l1=72, k2=26, l2=104, seed=4)
+    base = P.sparse_randomized_lu(P.Matrix.from_device(a), P.RandLuParams(**prm))
+    P.set_sketch_cache(True)
+    try:
+        r1 = P.sparse_randomized_lu(P.Matrix.from_device(a), P.RandLuParams(**prm))
+        s1 = P.sketch_cache_stats()
+        r2 = P.sparse_randomized_lu(P.Matrix.from_device(a), P.RandLuParams(**prm))
+        s2 = P.sketch_cache_stats()
+        assert s1["misses"] >= 2 and s2["hits"] >= s1["hits"] + 2 and s2["misses"] == s1["misses"]
+        for r in (r1, r2):
+            np.testing.assert_array_equal(r.P.indices, base.P.indices)
+            np.testing.assert_array_equal(r.Q.indices, base.Q.indices)
+            np.testing.assert_array_equal(r.L.numpy(), base.L.numpy())
+            np.testing.assert_array_equal(r.U.numpy(), base.U.numpy())
+        P.sparse_randomized_lu(P.Matrix.from_device(a), P.RandLuParams(**dict(prm, seed=6)))
+        assert P.sketch_cache_stats()["misses"] > s2["misses"]
+    finally:
+        P.set_sketch_cache(False)
+    assert P.sketch_cache_stats()["entries"] == 0
