@@ -96,6 +96,28 @@ __device__ inline void grid_arrive_wait(unsigned int *counter, unsigned int targ
     __syncthreads();
 }
 
+// The same barrier in two halves: arrive (all of the CTA's prior global
+// writes are published), then — after independent work — wait.
+__device__ inline void grid_arrive(unsigned int *counter) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+    }
+}
+
+__device__ inline void grid_wait(unsigned int *counter, unsigned int target) {
+    if (threadIdx.x == 0) {
+        unsigned int v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+            if ((int)(v - target) >= 0) break;
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+
 __device__ inline double ld_cg(const double *p) { return __ldcg(p); }
 
 // a / b correctly rounded (bit-identical to the IEEE division) from the

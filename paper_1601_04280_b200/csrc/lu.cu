@@ -95,6 +95,7 @@ struct LuParams {
     int64_t ldp;
     int l2pf;         // trailing update: L2 prefetch distance in warp passes (0 = off)
     int b2;           // outer block width (multiple of b, <= kLuB2Max; 0 = one level)
+    int la;           // priority-column look-ahead in the pivot steps (shared-memory panel)
 };
 
 __device__ inline bool better(unsigned long long a_abs, unsigned a_pos, unsigned long long b_abs,
@@ -322,7 +323,8 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     double *const spanel = reinterpret_cast<double *>(smem_raw);   // rpc x bs (GB == 0)
     double *PR = spanel + (GB ? 0 : (size_t)rpc * bs);              // b x b
     double *u = PR + (size_t)b * b;                                 // b
-    double *Ach = u + b;                                            // b x kLuXC
+    double *u2 = u + b;                                             // b (look-ahead: the previous step's pivot row)
+    double *Ach = u2 + b;                                           // b x kLuXC
     const int b2 = TWO ? p.b2 : 0;
     double *PRo = Ach + (size_t)b * kLuXC;                          // b2 x kLuB2Max
     double *Acho = PRo + (size_t)b2 * kLuB2Max;                     // b2 x kLuXC
@@ -330,6 +332,13 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
     int *pw_ent = pos + rpc;                                        // b
     int *pwo = pw_ent + b;                                          // b2: pivots of the outer block
     unsigned bar_target = 0;
+    // Priority-column look-ahead (shared-memory panel only): step ls updates
+    // only the next pivot column before the candidates of step ls+1 are
+    // published; the rest of its update (columns > ls+1) runs between the
+    // arrival at the grid barrier of step ls+1 and the wait on it.  The
+    // published candidate row gets that pending update on the fly, so every
+    // value is produced by the same operations in the same order.
+    const bool la = !GB && p.la != 0;
     LU_T0();
 
     // ---- thresh = PIVOT_RTOL * ||w||_F (deterministic two-level sum) ----
@@ -410,9 +419,12 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
         __syncthreads();
         LU_T(3);
 
+        bool pend_big = false;  // look-ahead: step ls-1 still owes columns > ls
         for (int ls = 0; ls < bw; ++ls) {
             const int s = J + ls;
             const int slot = s & 1;
+            double *const uc = (la && (ls & 1)) ? u2 : u;     // this step's pivot row
+            const double *const up = (ls & 1) ? u : u2;       // the previous step's (look-ahead)
             // 1. local candidate
             unsigned long long babs = 0ULL;
             unsigned bpos = 0xFFFFFFFFu;
@@ -460,10 +472,33 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 cs[blockIdx.x] = c;
             }
             if (bent >= 0)
-                for (int x = tid; x < bw; x += blockDim.x) crow[x] = panel[bent * es + x * xs];
+                for (int x = tid; x < bw; x += blockDim.x) {
+                    double v = panel[bent * es + x * xs];
+                    if (la && pend_big && x > ls) {  // the pending update of step ls-1, on the fly
+                        const double c = panel[bent * es + (ls - 1) * xs];
+                        v = MODE == MODE_ROW ? __dsub_rn(v, __dmul_rn(c, up[x]))
+                                             : __dsub_rn(v, __dmul_rn(up[x], c));
+                    }
+                    crow[x] = v;
+                }
             // 3. one grid barrier per pivot step
             bar_target += G;
-            grid_arrive_wait(p.bar, bar_target);
+            if (la) {
+                grid_arrive(p.bar);
+                if (pend_big) {  // step ls-1 on the columns > ls of the rows live at that step
+                    for (int e = tid; e < ne; e += blockDim.x) {
+                        if (pos[e] < s) continue;
+                        double *we = panel + e * bs;
+                        const double c = we[ls - 1];
+                        for (int x = ls + 1; x < bw; ++x)
+                            we[x] = MODE == MODE_ROW ? __dsub_rn(we[x], __dmul_rn(c, up[x]))
+                                                     : __dsub_rn(we[x], __dmul_rn(up[x], c));
+                    }
+                }
+                grid_wait(p.bar, bar_target);
+            } else {
+                grid_arrive_wait(p.bar, bar_target);
+            }
             LU_T(1);
             // 4. global winner
             {
@@ -479,7 +514,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 block_best(ga, gp, gc, s_abs, s_pos, s_ent);
                 if (tid == 0) s_wcta = gc;
                 const double *wrow = p.candrow + ((size_t)slot * G + gc) * k;
-                for (int x = tid; x < bw; x += blockDim.x) u[x] = __ldcg(wrow + x);
+                for (int x = tid; x < bw; x += blockDim.x) uc[x] = __ldcg(wrow + x);
                 if (tid == 0) {
                     pw_ent[ls] = __ldcg(&cs[gc].entity);
                     if (b2) pwo[s % b2] = pw_ent[ls];
@@ -490,10 +525,10 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
             LU_T(2);
             const int went = pw_ent[ls];
             const int wpos = (int)s_pos[1];
-            const double pivv = u[ls];
+            const double pivv = uc[ls];
             const bool big = fabs(pivv) > thresh;
             if (b < k)
-                for (int x = tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
+                for (int x = tid; x < bw; x += blockDim.x) PR[ls * b + x] = uc[x];
             // 5. swap positions s <-> wpos
             for (int e = tid; e < ne; e += blockDim.x) {
                 if (pos[e] == s) pos[e] = wpos;
@@ -525,7 +560,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                             we[ls * xs] = l;
 #pragma unroll
                             for (int x = 0; x < GB; ++x)
-                                if (x > ls && x < bw) we[x * xs] = __dsub_rn(v[r][x], __dmul_rn(l, u[x]));
+                                if (x > ls && x < bw) we[x * xs] = __dsub_rn(v[r][x], __dmul_rn(l, uc[x]));
                         } else {
                             we[ls * xs] = 0.0;
                         }
@@ -533,7 +568,7 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                 }
             } else if (GB) {
                 // multipliers of the pivot column: L[x] = u[x] / piv
-                for (int x = ls + 1 + tid; x < bw; x += blockDim.x) u[x] = big ? u[x] / pivv : 0.0;
+                for (int x = ls + 1 + tid; x < bw; x += blockDim.x) uc[x] = big ? uc[x] / pivv : 0.0;
                 __syncthreads();
                 for (int eb = tid; eb < ne; eb += RA * kLuThreads) {
                     double v[RA][GB > 0 ? GB : 1], cv[RA];
@@ -555,44 +590,48 @@ __global__ void __launch_bounds__(kLuThreads, 1) lu_kernel(LuParams p) {
                         if (isw[r]) {
 #pragma unroll
                             for (int x = 0; x < GB; ++x)
-                                if (x > ls && x < bw) we[x * xs] = u[x];
+                                if (x > ls && x < bw) we[x * xs] = uc[x];
                         } else if (act[r]) {
 #pragma unroll
                             for (int x = 0; x < GB; ++x)
-                                if (x > ls && x < bw) we[x * xs] = __dsub_rn(v[r][x], __dmul_rn(u[x], cv[r]));
+                                if (x > ls && x < bw) we[x * xs] = __dsub_rn(v[r][x], __dmul_rn(uc[x], cv[r]));
                         }
                     }
                 }
                 if (b < k)
-                    for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
+                    for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = uc[x];
             } else if (MODE == MODE_ROW) {
+                const int xend = la ? min(bw, ls + 2) : bw;   // look-ahead: the next pivot column only
                 for (int e = tid; e < ne; e += blockDim.x) {
                     if (pos[e] <= s) continue;
                     double *we = panel + e * bs;
                     if (big) {
                         const double l = we[ls] / pivv;
                         we[ls] = l;
-                        for (int x = ls + 1; x < bw; ++x) we[x] = __dsub_rn(we[x], __dmul_rn(l, u[x]));
+                        for (int x = ls + 1; x < xend; ++x) we[x] = __dsub_rn(we[x], __dmul_rn(l, uc[x]));
                     } else {
                         we[ls] = 0.0;
                     }
                 }
+                pend_big = la && big;
             } else {
                 // multipliers of the pivot column: L[x] = u[x] / piv
-                for (int x = ls + 1 + tid; x < bw; x += blockDim.x) u[x] = big ? u[x] / pivv : 0.0;
+                for (int x = ls + 1 + tid; x < bw; x += blockDim.x) uc[x] = big ? uc[x] / pivv : 0.0;
                 __syncthreads();
                 for (int e = tid; e < ne; e += blockDim.x) {
                     double *we = panel + e * bs;
                     if (e0 + e == went) {
-                        for (int x = ls + 1; x < bw; ++x) we[x] = u[x];
+                        for (int x = ls + 1; x < bw; ++x) we[x] = uc[x];
                         continue;
                     }
                     if (pos[e] <= s || !big) continue;
                     const double c = we[ls];
-                    for (int x = ls + 1; x < bw; ++x) we[x] = __dsub_rn(we[x], __dmul_rn(u[x], c));
+                    const int xend = la ? min(bw, ls + 2) : bw;
+                    for (int x = ls + 1; x < xend; ++x) we[x] = __dsub_rn(we[x], __dmul_rn(uc[x], c));
                 }
+                pend_big = la && big;
                 if (b < k)
-                    for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = u[x];
+                    for (int x = ls + 1 + tid; x < bw; x += blockDim.x) PR[ls * b + x] = uc[x];
             }
             __syncthreads();
             LU_T(6);
@@ -2152,6 +2191,10 @@ __global__ void __launch_bounds__(1024 / RPT, 1) lu_hybrid_kernel(LuHybridParams
             // block of trailing values — is loaded before the pivot-row
             // rounds below, so those latencies overlap.
             constexpr int NI = 3;
+            // the counter hand-off below lets cluster 0 start the next panel once
+            // pass 1 is done everywhere: pass 1 (columns x0 .. x0 + NI*4*ngrp - 1,
+            // ngrp >= 1) must therefore contain the whole next panel
+            static_assert(B <= NI * 4, "hybrid LU: pass 1 must cover the next panel's columns");
             const int ngrp = neT > 0 ? max(1, (int)blockDim.x / neT) : 1;
             const int el = neT > 0 ? tid % neT : 0, grp = neT > 0 ? tid / neT : ngrp;
             const int64_t e = eT0 + el;
@@ -2351,7 +2394,7 @@ static int lu_outer_width(int b, int64_t k, bool gpanel) {
 }
 
 static size_t lu_smem_bytes(int rpc, int b, int bs, int b2 = 0) {
-    return sizeof(double) * ((size_t)rpc * bs + (size_t)b * b + b + (size_t)b * kLuXC +
+    return sizeof(double) * ((size_t)rpc * bs + (size_t)b * b + 2 * (size_t)b + (size_t)b * kLuXC +
                              (size_t)b2 * kLuB2Max + (size_t)b2 * kLuXC) +
            sizeof(int) * ((size_t)rpc + b + b2) + 16;
 }
@@ -2588,6 +2631,8 @@ static int run_lu(double *w, int64_t M, int64_t k, int64_t ld, int64_t *perm, do
     prm.ldp = 0;
     prm.l2pf = 1;  // tools/lu_sweep.sh: config 3 LU(Y) 4.39 -> 4.08 ms
     prm.b2 = 0;
+    prm.la = 1;
+    if (const char *env = getenv("SRLU_LU_LA")) prm.la = atoi(env) != 0;  // testing knob
     if (const char *env = getenv("SRLU_LU_L2PF")) prm.l2pf = atoi(env);  // testing knob
 
     int rc = try_run_lu_hybrid<MODE>(prm, ws, stream);
