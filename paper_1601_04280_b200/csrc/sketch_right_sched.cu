@@ -223,6 +223,7 @@ __device__ __forceinline__ uint32_t pack_pair(uint32_t lo, uint32_t hi) {
 
 template <int PASS>
 __device__ __forceinline__ void sched_pass(const int32_t *src, int cnt, int g, int c, int nch,
+                                           int ch0, int ch1,
                                            int es8, int bpt, int d2, int joint, int32_t *np_tab,
                                            int32_t *wsched, uint32_t *codes, int32_t *header,
                                            unsigned *best, unsigned *best2) {
@@ -230,14 +231,25 @@ __device__ __forceinline__ void sched_pass(const int32_t *src, int cnt, int g, i
     const int ng = kGW * bpt;
     const int b = g / kGW, w = (b & 1) ? kGW - 1 - (g % kGW) : (g % kGW);
     const unsigned FULL = 0xffffffffu;
+    // chunks [ch0, ch1) of this group: the lane's first source at or beyond the
+    // first chunk's first column (its list is ascending in the column)
     int cur = 0;
-    int nxt = cnt > 0 ? src[0] : INT_MAX;
+    if (ch0 > 0) {
+        int lo = 0, hi = cnt;
+        const int c_first = ch0 * c;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((src[mid] & 0x7fffffff) < c_first) lo = mid + 1; else hi = mid;
+        }
+        cur = lo;
+    }
+    int nxt = cur < cnt ? src[cur] : INT_MAX;
     auto joint_np = [&](int ch, int ww) {  // common pairs of warp ww in chunk ch
         int mx = 0;
         for (int bb = 0; bb < bpt; ++bb) mx = max(mx, np_tab[ch * ng + group_of(ww, bb)]);
         return mx;
     };
-    for (int ch = 0; ch < nch; ++ch) {
+    for (int ch = ch0; ch < ch1; ++ch) {
         const int c0 = ch * c, c1 = c0 + c;
         uint32_t *out = nullptr;
         int npj = 0;
@@ -344,10 +356,13 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
                                                    const int32_t *__restrict__ grp,
                                                    int32_t *np_tab, int32_t *wsched,
                                                    uint32_t *codes, int32_t *header,
-                                                   unsigned *barrier) {
+                                                   unsigned *barrier, int cpb) {
     __shared__ unsigned best[32], best2[32];
     __shared__ int32_t lists[kSchedListCap];
-    const int g = blockIdx.x, lane = threadIdx.x;
+    // one warp per (group, slice of cpb chunks): blockIdx.x = slice * ng + group
+    const int ngrp = kGW * bpt;
+    const int g = blockIdx.x % ngrp, lane = threadIdx.x;
+    const int chq = (blockIdx.x / ngrp) * cpb, chr = min(nch, chq + cpb);
     const unsigned FULL = 0xffffffffu;
     const int t = grp ? grp[g * 32 + lane] : (g * 32 + lane < l ? g * 32 + lane : -1);
     const int beg = t >= 0 ? bptr[t] : 0;
@@ -372,10 +387,10 @@ __global__ void __launch_bounds__(32) sched_kernel(const int32_t *__restrict__ s
     best2[lane] = 0;
     __syncwarp();
     const int32_t *src = staged ? lists + off : sorted + beg;
-    sched_pass<0>(src, cnt, g, c, nch, es8, bpt, d2, joint, np_tab, wsched, codes, header, best,
+    sched_pass<0>(src, cnt, g, c, nch, chq, chr, es8, bpt, d2, joint, np_tab, wsched, codes, header, best,
                   best2);
     grid_arrive_wait(barrier, gridDim.x);
-    sched_pass<1>(src, cnt, g, c, nch, es8, bpt, d2, joint, np_tab, wsched, codes, header, best,
+    sched_pass<1>(src, cnt, g, c, nch, chq, chr, es8, bpt, d2, joint, np_tab, wsched, codes, header, best,
                   best2);
 }
 
@@ -813,11 +828,22 @@ extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, in
     int l_arg = (int)l1, c_arg = f.c, nch_arg = f.nch, es8 = es == 8, bpt_arg = f.bpt,
         d2_arg = f.d2, joint_arg = f.joint;
     unsigned *bar = (unsigned *)(header + 1);
+    // one warp per (group, slice of chunks): the simulation of a chunk only
+    // needs each lane's cursor at the chunk's first column (binary search),
+    // so the chunks of a group run in parallel — as many as stay co-resident
+    // (cooperative launch; config 2: 28 x 2 warps, 31 -> 17 us)
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    SRLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1s::sched_kernel, 32, 0));
+    int cpb = 1;
+    while ((int64_t)f.ng * ceil_div(f.nch, cpb) > (int64_t)per_sm * sms && cpb < f.nch) ++cpb;
+    const int nslices = (int)ceil_div(f.nch, cpb);
     void *args[] = {(void *)&sorted1, (void *)&bptr1, &l_arg,   &c_arg, &nch_arg, &es8,
                     &bpt_arg,         &d2_arg,        &joint_arg, (void *)&grp_arg, &np,
-                    &wsc,             &codes,         &header,  &bar};
-    SRLU_CUDA(cudaLaunchCooperativeKernel((const void *)k1s::sched_kernel, dim3(f.ng), dim3(32),
-                                          args, 0, s));
+                    &wsc,             &codes,         &header,  &bar, &cpb};
+    SRLU_CUDA(cudaLaunchCooperativeKernel((const void *)k1s::sched_kernel, dim3(f.ng * nslices),
+                                          dim3(32), args, 0, s));
     SRLU_CHECK_LAUNCH("k1s_sched_kernel");
     return SRLU_OK;
 }
