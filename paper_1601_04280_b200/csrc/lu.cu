@@ -22,6 +22,7 @@
 //     in-panel triangular recurrence.
 // Result: P/Q and L/U bit-identical to the reference on the same input.
 #include <cooperative_groups.h>
+#include <mutex>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -2403,10 +2404,13 @@ static size_t lu_smem_bytes(int rpc, int b, int bs, int b2 = 0) {
 }
 
 static int sm_count() {
+    static int cached = 0;   // one device per process (one process per GPU)
+    if (cached > 0) return cached;
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 1;
+    cached = n > 0 ? n : 1;
+    return cached;
 }
 
 // Cluster path when the panels of all M entities fit one cluster's shared
@@ -2457,9 +2461,13 @@ static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool
     const int k = prm.k;
     constexpr int CL = 16;
     auto kern = lu_hybrid_kernel<MODE, B, RPT>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-        cudaGetLastError();
-        return SRLU_OK;
+    static bool np_ok = false;   // set once per kernel variant
+    if (!np_ok) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            return SRLU_OK;
+        }
+        np_ok = true;
     }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
@@ -2480,10 +2488,25 @@ static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = nocoop ? 1 : 2;
-    // grid = every co-resident cluster (smem depends on the per-CTA range)
+    // grid = every co-resident cluster (smem depends on the per-CTA range).
+    // The occupancy search costs several driver queries (tens of
+    // microseconds of host time per LU): its result is kept for the last
+    // shape of this kernel variant.
+    struct Plan { int64_t M; int k; int nocoop; int ncl; size_t smem; };
+    static Plan last = {-1, 0, 0, 0, 0};
+    static std::mutex last_mu;
     int ncl = 0;
     size_t smem = 0;
-    for (int guess = 9; guess >= 1; --guess) {
+    bool cached = false;
+    {
+        std::lock_guard<std::mutex> lk(last_mu);
+        if (last.M == M && last.k == k && last.nocoop == nocoop) {
+            ncl = last.ncl;
+            smem = last.smem;
+            cached = true;   // the kernel's shared-memory attribute still holds this value
+        }
+    }
+    for (int guess = cached ? 0 : 9; guess >= 1; --guess) {
         const int rpcT = (int)ceil_div(M, (int64_t)(guess * CL));
         smem = lu_hybrid_smem_bytes<B>(rpcT, CL, k);
         if (smem > 220 * 1024) return SRLU_OK;
@@ -2500,6 +2523,13 @@ static int try_run_lu_hybrid_b(LuParams prm, void *ws, cudaStream_t stream, bool
             return SRLU_OK;
         }
         if (n >= guess) { ncl = guess; break; }
+    }
+    if (!cached) {
+        std::lock_guard<std::mutex> lk(last_mu);
+        last = {M, k, nocoop, ncl, smem};
+    } else {
+        cfg.gridDim = dim3(ncl * CL);
+        cfg.dynamicSmemBytes = smem;
     }
     if (ncl < 1 || ceil_div(M, (int64_t)CL) > 1024 ||
         ceil_div(M, (int64_t)(ncl * CL)) > 1024 / RPT)  // one entity per thread outside phase A
