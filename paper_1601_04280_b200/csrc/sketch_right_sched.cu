@@ -62,6 +62,17 @@ static int env_int(const char *name, int dflt) {
     return (s && *s) ? atoi(s) : dflt;
 }
 
+// SM count of the process's device (one process per GPU), queried once
+static int device_sms() {
+    static int cached = 0;
+    if (cached > 0) return cached;
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached = n > 0 ? n : 148;
+    return cached;
+}
+
 // Deterministic from (n, l, pad, es): the schedule and the kernel agree.
 // One geometry (rows per block rb, stage target bytes); false if it does
 // not fit the shared-memory budget with at least two stages.
@@ -726,10 +737,14 @@ static int launch(const Cfg &f, const T *a, int64_t m, int64_t n, int64_t lda,
     d.code_off = (int)(d.xs_off + f.xs_bytes);
     d.code_cap = (int)f.code_cap;
     auto kern = k1s_kernel<T, RB, BPT>;
-    SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // host time matters here (the stage-1 prologue is host-bound): the
+    // attribute is set again only when the size changes, the SM count once
+    static int64_t smem_set = -1;   // per kernel variant
+    if (smem_set != f.smem) {
+        SRLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem));
+        smem_set = f.smem;
+    }
+    const int sms = device_sms();
     const int64_t nrb = ceil_div(m, RB);
     const unsigned grid = (unsigned)(nrb < sms ? nrb : sms);
     kern<<<grid, kNT, (size_t)f.smem, s>>>(a, m, n, lda, ws, f.off_grp, f.off_wsched,
@@ -832,10 +847,10 @@ extern "C" int srlu_k1_schedule(const int32_t *sorted1, const int32_t *bptr1, in
     // needs each lane's cursor at the chunk's first column (binary search),
     // so the chunks of a group run in parallel — as many as stay co-resident
     // (cooperative launch; config 2: 28 x 2 warps, 31 -> 17 us)
-    int per_sm = 0, dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    SRLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1s::sched_kernel, 32, 0));
+    static int per_sm = 0;   // queried once
+    const int sms = k1s::device_sms();
+    if (per_sm == 0)
+        SRLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1s::sched_kernel, 32, 0));
     int cpb = 1;
     while ((int64_t)f.ng * ceil_div(f.nch, cpb) > (int64_t)per_sm * sms && cpb < f.nch) ++cpb;
     const int nslices = (int)ceil_div(f.nch, cpb);
