@@ -136,21 +136,17 @@ def test_tmem_k1_bit_exact(P, m, n, dt, l, k, rows, monkeypatch):
     np.testing.assert_array_equal(y.numpy(), ref)
 
 
-# K1-CSR: pad1 = 512 / 1024 take the register-resident kernel (k1_csr2_kernel),
-# other pads the shared-memory one; SRLU_K1_CSR_V1 forces the latter
-@pytest.mark.parametrize("m,n,l,k,dens,dt,v1", [
-    (3000, 4000, 600, 64, 0.01, np.float32, False),    # pad 1024, two blocks
-    (3000, 4000, 600, 64, 0.01, np.float32, True),
-    (1500, 2500, 300, 40, 0.02, np.float64, False),    # pad 512, one block
-    (700, 3000, 1000, 120, 0.05, np.float64, False),   # ~150 entries per row: several chunks, same-bucket lanes
-    (900, 5000, 200, 30, 0.01, np.float32, False),     # pad 256: shared-memory kernel
+# K1-CSR (warp per row): several pads, chunk counts and same-bucket collisions
+@pytest.mark.parametrize("m,n,l,k,dens,dt", [
+    (3000, 4000, 600, 64, 0.01, np.float32),     # pad 1024, two 512-point blocks
+    (1500, 2500, 300, 40, 0.02, np.float64),     # pad 512, one block
+    (700, 3000, 1000, 120, 0.05, np.float64),    # ~150 entries per row: several chunks, same-bucket lanes
+    (900, 5000, 200, 30, 0.01, np.float32),      # pad 256
 ])
-def test_csr_k1_bit_exact(P, m, n, l, k, dens, dt, v1, monkeypatch):
+def test_csr_k1_bit_exact(P, m, n, l, k, dens, dt):
     from scipy.sparse import random as sprandom
     from oracle import draws as D
     from oracle import randlu as O
-    if v1:
-        monkeypatch.setenv("SRLU_K1_CSR_V1", "1")
     g = np.random.Generator(np.random.Philox(100 + m))
     a = sprandom(m, n, density=dens, format="csr", random_state=g, dtype=np.float64)
     a.data = (g.standard_normal(a.nnz) * 10.0 ** g.integers(-12, 12, size=a.nnz)).astype(dt)
