@@ -116,11 +116,20 @@ def load(required_symbols: bool = True):
     return lib
 
 
+_cuda_checked = False
+
+
 def lib():
-    L = load()
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_1601_04280_b200 needs a CUDA device (B200, sm_100a); "
-                           "there is no CPU fallback")
+    """The loaded library; raises without a CUDA device (no CPU fallback).
+    The device check runs once: this is on the host-bound start of every
+    decomposition."""
+    global _cuda_checked
+    L = _lib if _lib is not None else load()
+    if not _cuda_checked:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1601_04280_b200 needs a CUDA device (B200, sm_100a); "
+                               "there is no CPU fallback")
+        _cuda_checked = True
     return L
 
 

@@ -369,7 +369,8 @@ def _composite_build(k, l, n, kind, seed, device, stream, k1_dtype, right):
     base = buf.data_ptr()
     staging = _STAGING.get(st_bytes)
     padc = ctypes.c_int64(0)
-    sh = _lib.stream_handle(stream)
+    cur = stream if stream is not None else torch.cuda.current_stream(dev)   # looked up once
+    sh = ctypes.c_void_p(cur.cuda_stream)
     P_ = ctypes.c_void_p
     if right is None:
         _lib.check(L.srlu_build_composite_k1(
@@ -393,7 +394,7 @@ def _composite_build(k, l, n, kind, seed, device, stream, k1_dtype, right):
             y.stride(0), P_(nonfinite.data_ptr()), sh),
             ("composite_sketch_right_dense_g" if off["grouped"] else "composite_sketch_right_dense")
             if sched_bytes else "composite_sketch_right_dense_nosched")
-    _STAGING.put(staging, stream if stream is not None else torch.cuda.current_stream(dev))
+    _STAGING.put(staging, cur)
     assert padc.value == pad
     isz = {torch.float64: 8, torch.int32: 4}
     view = lambda o, cnt, dt: buf[off[o]:off[o] + cnt * isz[dt]].view(dt)
