@@ -244,7 +244,10 @@ _LAYOUTS = {}
 def _composite_layout(L, k, l, n, k1_dtype):
     """Byte layout of one composite sketch (+ optional K1 schedule) in a
     single device buffer; cached per shape."""
-    key = (k, l, n, k1_dtype)
+    # the kernel-selection knobs change the schedule's size: part of the key
+    env = os.environ
+    key = (k, l, n, k1_dtype, env.get("SRLU_K1_TMEM"), env.get("SRLU_K1_NOSCHED"),
+           env.get("SRLU_K1_STAGE"), env.get("SRLU_K1_RB"))
     lay = _LAYOUTS.get(key)
     if lay is None:
         i4 = lambda c: ((c * 4 + 7) // 8) * 8
